@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""Benchmark: embedding-training samples/s of the fused TBE step on B200.
+
+N=1 workload = BASELINE config 2 (the metric's HBM-roofline bench): 64
+tables x 1,000,000 rows x dim 128 fp32, batch 65,536, pooling 32, row-wise
+AdaGrad (lr 0.05, eps 1e-8), upstream gradient = ones (the reference's
+sum-of-outputs loss, embedding.py:326).  A step = one fused TBE forward over
+all tables + one fused backward/row-wise-AdaGrad over all tables.
+
+N>1 (torchrun, one rank per GPU, NCCL): the sharded embedding step with the
+same per-GPU work (weak scaling): the 64 tables are placed table-wise by the
+reference planner's plan (tests/golden/plans), global batch 65,536 x N, and
+pooled rows / their gradients move through the all-to-all.
+
+--impl reference times the reference's CPU implementation of the same step
+(the oracle's port of the numpy code) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "embedding-training samples/sec"
+UNIT = "samples/s"
+LR, EPS = 0.05, 1e-8
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args(argv=None):
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--tables", type=int, default=64)
+    p.add_argument("--rows", type=int, default=1_000_000)
+    p.add_argument("--dim", type=int, default=128)
+    p.add_argument("--batch", type=int, default=65536, help="per-GPU batch (global = batch x N)")
+    p.add_argument("--pooling", type=int, default=32)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample-batch", type=int, default=0,
+                   help="samples per table in one CPU-baseline sample (default: full batch)")
+    return p.parse_args(argv)
+
+
+def workload_name(a) -> str:
+    return (f"c2: {a.tables} tables x {a.rows:,} rows x dim {a.dim} fp32, batch {a.batch:,}/GPU, "
+            f"pooling {a.pooling}, row-wise AdaGrad")
+
+
+def hbm_peak():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        try:
+            return float(json.loads(f.read_text())["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(index), "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, smax, reasons = [], [], set()
+        for line in out.splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for name, v in zip(self.NAMES, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes (SURVEY.md section 8d / DESIGN.md)
+
+
+def fwd_bytes(T, N, D, B, e=4, i=4, o=8):
+    """Compulsory bytes of one TBE forward: every lookup reads a row, ids,
+    offsets, pooled write."""
+    return T * (N * D * e + N * i + (B + 1) * o + B * D * 4)
+
+
+def bwd_bytes(U_list, N, D, B, e=4, i=4, o=8):
+    """Compulsory bytes of the fused backward + row-wise AdaGrad: upstream
+    read, ids, offsets, read+write of every touched row and its moment."""
+    return sum(B * D * 4 + N * i + (B + 1) * o + U * (2 * D * e + 2 * 4) for U in U_list)
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline (oracle port of the reference numpy code) — checker only
+
+
+def _cpu_worker(args):
+    table_seed, H, D, n, L, reps = args
+    from oracle import tbe_oracle as O
+
+    rng = np.random.default_rng(table_seed)
+    values = rng.standard_normal((H, D))
+    moment = np.zeros(H)
+    lengths = np.full(n, L, dtype=np.int64)
+    times = []
+    for r in range(reps):
+        idx = rng.integers(0, H, size=n * L, dtype=np.int64)
+        t0 = time.perf_counter()
+        O.np_forward_pooled(values, lengths, idx)
+        ids, g = O.np_backward_sort_aggregate(lengths, idx, np.ones((n, D)))
+        O.np_apply("rowwise_adagrad", values, moment, ids, g, LR, EPS)
+        times.append(time.perf_counter() - t0)
+    return times
+
+
+def cpu_procs(H, D, n, L, limit=None) -> int:
+    per_proc = H * D * 8 + 3 * n * L * D * 8 + (1 << 29)
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 16 << 30
+    cores = os.cpu_count() or 1
+    p = max(1, min(cores, int(avail * 0.7 // per_proc)))
+    return min(p, limit) if limit else p
+
+
+class CpuPool:
+    """Table-parallel pool: one reference-port table step per process."""
+
+    def __init__(self, procs):
+        import multiprocessing as mp
+
+        self.procs = procs
+        self.pool = mp.get_context("spawn").Pool(procs)
+
+    def run(self, H, D, n, L, reps, seed0=0):
+        jobs = [(seed0 + k, H, D, n, L, reps) for k in range(self.procs)]
+        t0 = time.perf_counter()
+        res = self.pool.map(_cpu_worker, jobs)
+        return res, time.perf_counter() - t0
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_baseline(a, T_total) -> dict:
+    n = a.cpu_sample_batch or a.batch
+    procs = cpu_procs(a.rows, a.dim, n, a.pooling, limit=T_total)
+    pool = CpuPool(procs)
+    res, _ = pool.run(a.rows, a.dim, n, a.pooling, 1)
+    pool.close()
+    t_table = max(r[0] for r in res)  # one table per process, in parallel
+    rounds = math.ceil(T_total / procs)
+    step_s = t_table * rounds * (a.batch / n)
+    return {"value": a.batch / step_s, "unit": UNIT, "cores": procs, "kind": "port",
+            "sample": f"{procs} of {T_total} tables (one per process), {n:,} samples x {a.pooling} ids each, "
+                      f"fwd+sort-aggregate+row-wise AdaGrad with the reference's numpy primitives "
+                      f"(oracle/tbe_oracle.py np_*); step time = max table time x {rounds} rounds"
+                      + (f" x {a.batch // n} batch scale" if n != a.batch else ""),
+            "table_s": t_table}
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the reference's CPU implementation (oracle port),
+    all host cores, rank 0 only."""
+    if rank != 0:
+        return
+    n = a.cpu_sample_batch or max(a.batch // 8, 1)
+    procs = cpu_procs(a.rows, a.dim, n, a.pooling, limit=a.tables)
+    pool = CpuPool(procs)
+    rounds = math.ceil(a.tables / procs)
+    scale = a.batch / n
+    for _ in range(a.warmup):
+        pool.run(a.rows, a.dim, n, a.pooling, 1, seed0=100)
+    steps = []
+    for k in range(a.steps):
+        res, _ = pool.run(a.rows, a.dim, n, a.pooling, 1, seed0=1000 + k)
+        steps.append(max(r[0] for r in res) * rounds * scale)
+    pool.close()
+    ms = 1e3 * float(np.mean(steps))
+    value = a.batch * world / (ms / 1e3) if world > 1 else a.batch / (ms / 1e3)
+    sample = (f"per step: {procs} of {a.tables} tables in parallel (one per process), {n:,} samples x "
+              f"{a.pooling} ids each; step time scaled x{rounds} rounds x{scale:g} batch")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(a), "tables": a.tables, "rows": a.rows, "dim": a.dim,
+                       "batch_per_gpu": a.batch, "pooling": a.pooling},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def count_launches(step_fn) -> int:
+    """Kernels launched by one step, from a CUPTI trace of an untimed step."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        step_fn()
+        torch.cuda.synchronize()
+    n = 0
+    for ev in prof.events():
+        if getattr(ev, "device_type", None) is not None and "CUDA" in str(ev.device_type):
+            name = ev.name
+            if "Memcpy" in name or "Memset" in name:
+                continue
+            n += 1
+    return n
+
+
+def run_b200(a, rank, world):
+    import torch
+
+    from paper_2104_05158_b200 import tbe
+    import paper_2104_05158_b200 as neo
+
+    neo.load()
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    if world > 1:
+        from paper_2104_05158_b200 import dist as ndist
+
+        return ndist.bench_sharded(a, rank, world, dev)
+    T, H, D, B, L = a.tables, a.rows, a.dim, a.batch, a.pooling
+    N = B * L
+    torch.manual_seed(0)
+    grp = tbe.TableGroup([H] * T, [D] * T, dtype=torch.float32, optim="rowwise_adagrad", device=dev)
+    grp._storage.normal_()
+    offsets = torch.arange(0, T * B + 1, dtype=torch.int64, device=dev) * L
+    batches = [torch.randint(0, H, (T * N,), dtype=torch.int32, device=dev) for _ in range(2)]
+    out = torch.empty((B, T * D), dtype=torch.float32, device=dev)
+    upstream = torch.ones((B, T * D), dtype=torch.float32, device=dev)
+    U_list = [int(torch.unique(batches[0][t * N:(t + 1) * N]).numel()) for t in range(T)]
+
+    def step(i):
+        ix = batches[i % 2]
+        grp.forward(ix, offsets, B, out=out)
+        grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS)
+
+    for i in range(a.warmup):
+        step(i)
+    launches_per_step = count_launches(lambda: step(0))
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    clocks = Clocks(dev.index)
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    for i in range(a.steps):
+        e0, e1, e2 = ev[i]
+        e0.record()
+        ix = batches[i % 2]
+        grp.forward(ix, offsets, B, out=out)
+        e1.record()
+        grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS)
+        e2.record()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = ev[0][0].elapsed_time(ev[-1][2])
+    fwd_ms = float(np.mean([e0.elapsed_time(e1) for e0, e1, _ in ev]))
+    bwd_ms = float(np.mean([e1.elapsed_time(e2) for _, e1, e2 in ev]))
+    ms = total_ms / a.steps
+    peak, peak_kind = hbm_peak()
+    fb, bb = fwd_bytes(T, N, D, B), bwd_bytes(U_list, N, D, B)
+    fwd_gbs = fb / (fwd_ms * 1e-3) / 1e9
+    bwd_gbs = bb / (bwd_ms * 1e-3) / 1e9
+    step_gbs = (fb + bb) / (ms * 1e-3) / 1e9
+    dominant = ("tbe_forward_kernel", fwd_gbs, fb, fwd_ms) if fwd_ms >= bwd_ms else \
+        ("tbe_backward (keys+sort+segments+row-wise AdaGrad)", bwd_gbs, bb, bwd_ms)
+    line = {
+        "metric": METRIC, "value": B / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(a), "tables": T, "rows": H, "dim": D, "batch_per_gpu": B,
+                   "pooling": L, "index_dtype": "int32", "optimizer": "rowwise_adagrad",
+                   "l2": "inputs larger than L2 (32.8 GB of tables, 537 MB of ids per step, 2 alternating batches)"},
+        "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": dominant[1], "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": dominant[1] / peak,
+                     "traffic": None, "algorithmic_bytes": dominant[2], "ms": dominant[3]},
+        "roofline_step": {"achieved": step_gbs, "frac": step_gbs / peak, "fwd_gbs": fwd_gbs, "bwd_gbs": bwd_gbs,
+                          "fwd_ms": fwd_ms, "bwd_ms": bwd_ms, "bytes": fb + bb,
+                          "unique_rows_per_table": float(np.mean(U_list))},
+        "gpu_launches": launches_per_step * a.steps,
+        "clocks": clk,
+    }
+    if not a.no_e2e:
+        line["e2e"] = e2e_b200(a, grp, dev)
+    if not a.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(a, T)
+    print(json.dumps(line), flush=True)
+
+
+def e2e_b200(a, grp, dev) -> dict:
+    """Same step through the public pipeline API with host (pinned) inputs:
+    every step copies its ids/offsets H2D and reads the loss back D2H."""
+    import torch
+
+    from paper_2104_05158_b200.pipeline import TrainPipeline
+
+    T, H, D, B, L = a.tables, a.rows, a.dim, a.batch, a.pooling
+    N = B * L
+    g = torch.Generator().manual_seed(1)
+    host = [torch.randint(0, H, (T * N,), dtype=torch.int32, generator=g).pin_memory() for _ in range(2)]
+    lengths = torch.full((T * B,), L, dtype=torch.int64).pin_memory()
+    pipe = TrainPipeline(grp, batch=B, optim="rowwise_adagrad", lr=LR, eps=EPS)
+    batches = [(lengths, host[i % 2]) for i in range(a.warmup + a.steps)]
+    pipe.run(batches[:a.warmup])
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    losses = pipe.run(batches[a.warmup:])
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / a.steps
+    assert len(losses) == a.steps
+    return {"value": B / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": host[0].numel() * 4 + lengths.numel() * 8, "d2h_bytes_per_step": 8,
+            "api": "paper_2104_05158_b200.pipeline.TrainPipeline.run (pinned host ids/lengths, "
+                   "H2D prefetch overlapped with the previous step, loss = sum of pooled outputs read back)"}
+
+
+def main(argv=None):
+    a = parse_args(argv)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world != a.gpus and world > 1:
+        print(f"warning: WORLD_SIZE={world} but --gpus {a.gpus}", file=sys.stderr)
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+    return run_b200(a, rank, world)
+
+
+if __name__ == "__main__":
+    main()

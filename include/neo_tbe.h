@@ -1,0 +1,221 @@
+/*
+ * neo_tbe.h — C ABI of libneob200.so, the B200-native hot path of Neo
+ * (arXiv 2104.05158): table-batched embedding-bag (TBE) forward, the
+ * sort/segment-reduce backward fused with the sparse optimizer, row-wise
+ * bucketisation, the (W,T,B)<->(T,W,B) block permute and the pooled-row
+ * piece copies used around the all-to-all.
+ *
+ * Every entry point is stream-ordered and asynchronous: all buffers are
+ * caller-allocated DEVICE memory unless a parameter says "host"; the library
+ * never allocates and never synchronises on the success path.  Return value
+ * is a status code (NEO_OK or NEO_E_*): argument errors are detected on the
+ * host before any launch; data errors (an out-of-range row id) are recorded
+ * on the device in a caller-provided neo_error record that the caller reads
+ * after the stream completes.  neo_last_error() returns a thread-local
+ * message for the last non-OK status.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/neosim):
+ *   neo_tbe_forward            embedding.py:136-151 forward_pooled,
+ *                              embedding.py:154-168 fused_forward
+ *   neo_tbe_backward (AGGREGATE) embedding.py:175-192 backward_sort_aggregate
+ *   neo_tbe_backward (UPDATE)  embedding.py:270-281 fused_backward_update
+ *                              (+ embedding.py:212-254 the three optimizers)
+ *   neo_tbe_backward (DENSE)   embedding.py:195-205 merge_row_gradients input
+ *                              (dense DP gradient for the all-reduce)
+ *   neo_apply_row_updates      embedding.py:212-267 apply_rowwise_adagrad /
+ *                              apply_adagrad / apply_sgd / apply_optimizer
+ *   neo_fp16_roundtrip         embedding.py:288-305 quantize_fp16_roundtrip,
+ *                              storage_roundtrip
+ *   neo_cast                   comms.py:521-540 quantized communication
+ *                              (fp16 fwd / bf16 bwd payloads)
+ *   neo_lengths_to_offsets     model.py:365-370 lengths_to_offsets
+ *   neo_bucketize_rowwise      comms.py:107-141 bucketize_rowwise
+ *   neo_permute_blocks         comms.py:222-257 permute_WTB_to_TWB /
+ *                              permute_TWB_to_WTB (and to_wtb, comms.py:197)
+ *   neo_copy_pieces            comms.py:692-711 pooled assembly (TW copy,
+ *                              CW column placement, RW partial sum)
+ *   neo_gather_blocks          comms.py:292-353 alltoall_redistribute send
+ *                              packing; comms.py:164-172 replicate_columnwise
+ */
+#ifndef NEO_TBE_H
+#define NEO_TBE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------- */
+enum {
+  NEO_OK = 0,
+  NEO_E_INDEX_RANGE = 1, /* errors.py:43 IndexOutOfRange  */
+  NEO_E_LAYOUT = 2,      /* errors.py:50 LayoutMismatch   */
+  NEO_E_ARG = 3,         /* errors.py:18 InvalidValue     */
+  NEO_E_CUDA = 4         /* launch / runtime failure      */
+};
+
+/* ---- element types --------------------------------------------------- */
+enum { NEO_F32 = 0, NEO_F16 = 1, NEO_F64 = 2, NEO_BF16 = 3 };
+enum { NEO_I32 = 0, NEO_I64 = 1 };
+enum { NEO_POOL_SUM = 0, NEO_POOL_MEAN = 1 };
+/* embedding.py:24-27 OptimizerKind */
+enum { NEO_OPT_SGD = 0, NEO_OPT_ROWWISE_ADAGRAD = 1, NEO_OPT_ADAGRAD = 2, NEO_OPT_NONE = 3 };
+/* backward modes */
+enum {
+  NEO_BWD_UPDATE = 0,    /* aggregate + exactly one optimizer step per touched row */
+  NEO_BWD_AGGREGATE = 1, /* emit RowGradients (ids ascending, grads) only */
+  NEO_BWD_DENSE = 2      /* write aggregated rows into dense per-table gradients */
+};
+
+/* Device-side error record (caller allocates sizeof(neo_error) bytes of
+ * device memory).  position = first offending position in index-buffer
+ * order (INT64_MAX when clean), value = the offending row id, table = the
+ * table (or bag group) it belongs to. */
+typedef struct neo_error {
+  int64_t position;
+  int64_t value;
+  int32_t table;
+  int32_t code;
+} neo_error;
+
+int neo_version(void);
+const char* neo_last_error(void);
+/* number of SMs of the current device (0 if no device) */
+int neo_device_sm_count(void);
+int neo_error_reset(neo_error* err, void* stream);
+
+/* ---- TBE forward (embedding.py:136-168) -------------------------------
+ * T tables, B bags per table.  Bag (t, b) covers positions
+ * offsets[t*B+b] .. offsets[t*B+b+1] of the concatenated index buffer
+ * (model.py:301-337 CombinedBatch: table-major, then sample-major).
+ * Table t: rows row_offsets[t+1]-row_offsets[t], dim dim_offsets[t+1]-
+ * dim_offsets[t], values at weights[t] (row-major, weight_dtype).
+ * out[b*out_stride + dim_offsets[t] + j] = sum over the bag (SUM) or the bag
+ * mean (MEAN; empty bag -> 0).  F64 weights accumulate in f64, sequentially in
+ * buffer order (bit-identical to np.add.at); F32/F16 accumulate in f32. */
+int neo_tbe_forward(int32_t num_tables, int64_t batch,
+                    const int64_t* row_offsets,  /* [T+1] */
+                    const int32_t* dim_offsets,  /* [T+1] */
+                    int32_t max_dim,
+                    const uint64_t* weights,     /* [T] device pointers */
+                    int32_t weight_dtype,
+                    const void* indices, int32_t index_dtype,
+                    const int64_t* offsets,      /* [T*B+1] */
+                    int32_t pooling,
+                    void* out, int32_t out_dtype, int64_t out_stride,
+                    neo_error* err,              /* may be NULL */
+                    void* stream);
+
+/* ---- TBE backward (embedding.py:175-281) ------------------------------
+ * Sort (table row, bag) pairs stably by row, run-length segment them, then
+ * one warp per touched row sums the upstream rows of its occurrences in
+ * buffer order and, in UPDATE mode, applies exactly one optimizer step in
+ * place (no dense gradient is materialised).
+ *   grad: upstream gradient, row b of table t at grad[b*grad_stride +
+ *         dim_offsets[t] ..], grad_dtype F32/BF16/F16 (F64 with F64 weights)
+ *   moments[t]: row-wise (H_t) or element-wise (H_t x D_t) state, f32 for
+ *         F32/F16 weights, f64 for F64 weights; ignored for SGD
+ *   AGGREGATE: out_ids[u] = row_offsets[t] + row (ascending), out_grads
+ *         (U x max_dim, accumulator type), *out_count = U (device int64)
+ *   DENSE: dense_grads[t] (H_t x D_t, accumulator type, pre-zeroed) get the
+ *         aggregated rows.
+ * Workspace size: neo_tbe_backward_workspace_bytes. */
+size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows);
+
+int neo_tbe_backward(int32_t num_tables, int64_t batch,
+                     const int64_t* row_offsets, int64_t total_rows,
+                     const int32_t* dim_offsets, int32_t max_dim,
+                     const uint64_t* weights, int32_t weight_dtype,
+                     const uint64_t* moments,      /* [T] or NULL */
+                     const void* indices, int32_t index_dtype,
+                     const int64_t* offsets, int64_t num_indices,
+                     int32_t pooling,
+                     const void* grad, int32_t grad_dtype, int64_t grad_stride,
+                     int32_t mode, int32_t optim, double lr, double eps,
+                     int64_t* out_ids, void* out_grads, int64_t* out_count,
+                     const uint64_t* dense_grads,  /* [T] or NULL */
+                     void* workspace, size_t workspace_bytes,
+                     neo_error* err, void* stream);
+
+/* ---- sparse optimizer from RowGradients (embedding.py:212-267) ---------
+ * ids: n row ids (NULL = rows 0..n-1, the dense-gradient case);
+ * grads: n x dim in the accumulator type of weight_dtype (f64 for F64,
+ * else f32).  Rows whose gradient is identically zero are skipped for the
+ * AdaGrad variants (embedding.py:225-228). */
+int neo_apply_row_updates(int64_t n, const int64_t* ids, const void* grads,
+                          int32_t dim, void* weight, int32_t weight_dtype,
+                          void* moment, int32_t optim, double lr, double eps,
+                          void* stream);
+
+/* ---- precision (embedding.py:288-305, comms.py:521-540) --------------- */
+/* x (f64, n) -> RNE through binary16 -> f64 in place; overflow[i] = 1 where
+ * the result is +-inf (may be NULL); *nonfinite (device int32, may be NULL)
+ * set to 1 when an input is non-finite. */
+int neo_fp16_roundtrip(int64_t n, double* x, uint8_t* overflow, int32_t* nonfinite,
+                       void* stream);
+/* element-wise RNE conversion between NEO_F32/F16/BF16/F64 */
+int neo_cast(int64_t n, const void* src, int32_t src_dtype, void* dst, int32_t dst_dtype,
+             void* stream);
+
+/* ---- jagged metadata (model.py:365-370) -------------------------------- */
+int neo_lengths_to_offsets(int64_t n, const int64_t* lengths, int64_t* offsets /* n+1 */,
+                           void* workspace, size_t workspace_bytes, void* stream);
+size_t neo_scan_workspace_bytes(int64_t n);
+
+/* ---- row-wise bucketisation (comms.py:107-141) -------------------------
+ * n bags with offsets[n+1] over indices; shard s owns rows
+ * [shard_starts[s], shard_starts[s+1]) (k+1 host values, tiling [0,H)).
+ * Outputs: out_lengths (k x n, shard-major), out_offsets (k*n+1, exclusive
+ * scan of out_lengths: shard s occupies out_indices[out_offsets[s*n] ..
+ * out_offsets[(s+1)*n])), out_indices (N, rebased to the shard, original
+ * order kept inside each shard).  Bit-exact. */
+size_t neo_bucketize_workspace_bytes(int64_t n, int32_t k);
+int neo_bucketize_rowwise(int64_t n, const int64_t* offsets, const void* indices,
+                          int32_t index_dtype, int32_t k, const int64_t* shard_starts_host,
+                          int64_t* out_lengths, int64_t* out_offsets, void* out_indices,
+                          int32_t table, neo_error* err,
+                          void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- block permute (comms.py:222-264) ----------------------------------
+ * lengths: outer*inner*B entries whose (o, i) block of B lengths covers the
+ * next sum(lengths) indices; output is the (i, o) block order.  WTB->TWB is
+ * outer=W, inner=T; TWB->WTB is outer=T, inner=W. */
+size_t neo_permute_workspace_bytes(int32_t outer, int32_t inner);
+int neo_permute_blocks(int32_t outer, int32_t inner, int64_t B,
+                       const int64_t* lengths, const void* indices, int32_t index_dtype,
+                       int64_t* out_lengths, void* out_indices,
+                       void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- pooled-row pieces (comms.py:692-711) ------------------------------
+ * For r in [0, rows): dst[r*dst_stride + dst_col + j] (=|+=) cast(src[r*
+ * src_stride + src_col + j]) for j < width, pieces applied in array order
+ * (so RW partial pools add in shard order).  pieces: device array of
+ * neo_piece.  src/dst dtypes F32/F16/BF16/F64. */
+typedef struct neo_piece {
+  uint64_t src;        /* device pointer */
+  uint64_t dst;        /* device pointer */
+  int64_t src_stride;  /* elements */
+  int64_t dst_stride;  /* elements */
+  int32_t src_col;
+  int32_t dst_col;
+  int32_t width;
+  int32_t accumulate;  /* 0 = overwrite, 1 = add */
+} neo_piece;
+int neo_copy_pieces(int64_t rows, const neo_piece* pieces, int32_t num_pieces,
+                    int32_t src_dtype, int32_t dst_dtype, void* stream);
+
+/* ---- block gather (comms.py:292-353 send packing, comms.py:164-172) ----
+ * dst[dst_off[i] .. dst_off[i]+count[i]) = src_ptr[i][0 .. count[i]) for
+ * each of n blocks; elem_bytes 4 or 8 (indices, lengths).  Blocks are
+ * device arrays. */
+int neo_gather_blocks(int32_t n, const uint64_t* src_ptrs, const int64_t* counts,
+                      const int64_t* dst_offsets, void* dst, int32_t elem_bytes,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEO_TBE_H */

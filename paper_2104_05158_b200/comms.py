@@ -1,0 +1,188 @@
+"""Reference-facing input redistribution and sharded step, on the B200.
+
+Mirrors neosim/comms.py: same names, signatures and error behaviour.  The
+integer layout work (bucketize, block permute, replication, send packing)
+runs in libneob200's bit-exact kernels; the sharded step runs the same
+per-rank pipeline as the NCCL path (``dist.py``) with W logical ranks on
+one GPU (``dist.LocalComm``), so the reference's W-worker equivalence tests
+exercise the production exchange logic.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import tbe
+from .errors import IndexOutOfRange, InvalidValue, LayoutMismatch
+from .spec import CombinedBatch, GlobalBatchLayout, LayoutTag
+
+LENGTH_BYTES = 8  # comms.py:47 lengths travel as int64 in the metadata phase
+
+
+def _device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2104_05158_b200 operators require a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _dev(a) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a)).to(_device())
+
+
+# ---------------------------------------------------------------------------
+# bucketize / replicate (comms.py:107-172)
+
+
+def bucketize_rowwise(lengths, indices, boundaries: Sequence, table_id: str = ""):
+    """Route each id to the row shard containing it, rebased; per-shard
+    lengths recomputed; order kept inside each shard (comms.py:107-141)."""
+    lengths = np.asarray(lengths, dtype=np.int64)
+    indices = np.asarray(indices, dtype=np.int64)
+    if int(lengths.sum()) != len(indices):
+        raise LayoutMismatch("lengths do not cover the index buffer")
+    pos = 0
+    for a, b in boundaries:
+        if a != pos or b <= a:
+            raise InvalidValue("boundaries", "must tile [0, H) in order")
+        pos = b
+    starts = [int(a) for a, _ in boundaries] + [pos]
+    k, n = len(boundaries), len(lengths)
+    if n == 0:
+        return [(np.zeros(0, np.int64), np.zeros(0, np.int64)) for _ in range(k)]
+    err = tbe.ErrorRecord(_device()).reset()
+    off = tbe.lengths_to_offsets(_dev(lengths))
+    out_len, out_off, out_idx = tbe.bucketize_rowwise(off, _dev(indices), starts, err=err)
+    r = err.read()
+    if r is not None:
+        raise IndexOutOfRange(table_id, r[1])
+    L = out_len.cpu().numpy()
+    O = out_off.cpu().numpy()
+    I = out_idx.cpu().numpy()
+    return [(L[s].copy(), I[O[s * n]:O[(s + 1) * n]].copy()) for s in range(k)]
+
+
+def replicate_columnwise(lengths, indices, num_col_shards: int):
+    """k byte-identical input copies (comms.py:164-172).  The NCCL path
+    never materialises them: one send buffer feeds every column shard."""
+    if num_col_shards < 1:
+        raise InvalidValue("num_col_shards", "must be >= 1")
+    lengths = np.asarray(lengths, dtype=np.int64)
+    indices = np.asarray(indices, dtype=np.int64)
+    out = []
+    for src in (lengths, indices):
+        if src.size == 0:
+            out.append([src.copy() for _ in range(num_col_shards)])
+            continue
+        d = _dev(src)
+        rep = torch.empty(num_col_shards * src.size, dtype=d.dtype, device=d.device)
+        tbe.gather_blocks([d] * num_col_shards, [src.size] * num_col_shards, rep)
+        h = rep.cpu().numpy().reshape(num_col_shards, src.size)
+        out.append([h[i].copy() for i in range(num_col_shards)])
+    return list(zip(out[0], out[1]))
+
+
+# ---------------------------------------------------------------------------
+# laid-out batches and the block permute (comms.py:175-264)
+
+
+@dataclass(frozen=True)
+class LaidOutBatch:
+    layout: GlobalBatchLayout
+    lengths: np.ndarray
+    indices: np.ndarray
+
+    def __post_init__(self):
+        lay = self.layout
+        expected = lay.workers * lay.tables * lay.local_batch
+        if len(self.lengths) != expected:
+            raise LayoutMismatch(f"expected {expected} length entries, got {len(self.lengths)}")
+        if int(np.sum(self.lengths)) != len(self.indices):
+            raise LayoutMismatch("lengths do not cover the index buffer")
+
+
+def _permute(lengths, indices, outer: int, inner: int, B: int):
+    lengths = np.asarray(lengths, dtype=np.int64)
+    indices = np.asarray(indices, dtype=np.int64)
+    if lengths.size == 0 or B == 0:
+        return lengths.copy(), indices.copy()
+    if indices.size == 0:
+        L, _ = tbe.permute_blocks(outer, inner, B, _dev(lengths), torch.zeros(1, dtype=torch.int64, device=_device()))
+        return L.cpu().numpy(), indices.copy()
+    L, I = tbe.permute_blocks(outer, inner, B, _dev(lengths), _dev(indices))
+    return L.cpu().numpy(), I.cpu().numpy()
+
+
+def _tag(t):
+    return getattr(t, "value", t)
+
+
+def _permute_laid(laid, new_tag: LayoutTag):
+    lay = laid.layout
+    W, T, B = lay.workers, lay.tables, lay.local_batch
+    outer, inner = (W, T) if _tag(lay.tag) == "WTB" else (T, W)
+    L, I = _permute(laid.lengths, laid.indices, outer, inner, B)
+    return LaidOutBatch(GlobalBatchLayout(W, T, B, new_tag), L, I)
+
+
+def permute_WTB_to_TWB(laid) -> LaidOutBatch:
+    """comms.py:248-252"""
+    if _tag(laid.layout.tag) != "WTB":
+        raise LayoutMismatch("expected WTB layout")
+    return _permute_laid(laid, LayoutTag.TWB)
+
+
+def permute_TWB_to_WTB(laid) -> LaidOutBatch:
+    """comms.py:255-258"""
+    if _tag(laid.layout.tag) != "TWB":
+        raise LayoutMismatch("expected TWB layout")
+    return _permute_laid(laid, LayoutTag.WTB)
+
+
+def to_wtb(batch, workers: int) -> LaidOutBatch:
+    """Canonical batch -> (W, T, B) wire order (comms.py:197-219).  The
+    canonical buffer is already the (T, W, B) block order, so this is one
+    device block permute."""
+    if workers < 1 or batch.num_samples % workers:
+        raise LayoutMismatch("workers must divide the global sample count")
+    T, B = batch.num_tables, batch.num_samples // workers
+    L, I = _permute(np.asarray(batch.lengths).reshape(-1), batch.indices, T, workers, B)
+    return LaidOutBatch(GlobalBatchLayout(workers, T, B, LayoutTag.WTB), L, I)
+
+
+def from_twb(laid) -> CombinedBatch:
+    """comms.py:261-264"""
+    if _tag(laid.layout.tag) != "TWB":
+        raise LayoutMismatch("expected TWB layout")
+    lay = laid.layout
+    return CombinedBatch(np.asarray(laid.lengths).reshape(lay.tables, lay.workers * lay.local_batch),
+                         laid.indices)
+
+
+# ---------------------------------------------------------------------------
+# redistribution results (comms.py:271-285)
+
+
+@dataclass
+class ShardInput:
+    table_id: str
+    shard: object
+    lengths: np.ndarray
+    indices: np.ndarray
+    sample_base: int = 0
+
+
+@dataclass
+class WorkerSlice:
+    worker: int
+    inputs: list = field(default_factory=list)
+
+
+@dataclass
+class ShardedState:
+    """comms.py:605-610"""
+
+    shards: dict
+    dp_replicas: dict

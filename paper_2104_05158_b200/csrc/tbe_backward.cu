@@ -1,0 +1,454 @@
+// TBE backward fused with the sparse optimizer.
+//
+// Reference semantics:
+//   embedding.py:175-192 backward_sort_aggregate — ids = unique(indices)
+//     ascending; grads[r] = sum over r's occurrences (duplicates counted per
+//     occurrence) of upstream[sample], summed in buffer order (np.add.at).
+//   embedding.py:212-232 apply_rowwise_adagrad — rows with an identically
+//     zero gradient are skipped; m_r += mean_j g_rj^2 (numpy pairwise sum);
+//     w_rj -= (lr * g_rj) / (sqrt(m_r) + eps).
+//   embedding.py:235-254 apply_adagrad / apply_sgd; embedding.py:270-281
+//     fused_backward_update = aggregate, then exactly ONE optimizer
+//     application per touched row.
+//
+// B200 mapping (one launch sequence for all T tables of a group):
+//   1. key build: warp per bag writes (key = row_offsets[t] + id, bag) pairs
+//      for its occurrences (coalesced), range-checking ids;
+//   2. stable LSD radix sort of the pairs on ceil(log2(total_rows+1)) bits
+//      (keys are table-major, so each table's rows are contiguous and each
+//      table's upstream slice stays L2-resident while its rows are updated);
+//   3. segment heads (key[i] != key[i-1]) compacted into segment starts;
+//   4. persistent segment kernel: one warp per touched row sums the upstream
+//      rows of its occurrences in sorted (= buffer) order into a warp-private
+//      shared-memory row, then applies the optimizer to the weight row and
+//      its moment in place.  No dense gradient is ever materialised.
+// F64 tables run the identical sequence with f64 accumulation, numpy's
+// pairwise order for the row mean and no FMA contraction, so results are
+// bit-identical to the reference.
+#include <climits>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
+#include "common.cuh"
+#include "optim.cuh"
+
+namespace neo {
+
+constexpr int kBwdWarps = 8;
+constexpr int kBwdUnroll = 8;
+
+static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static inline int key_bits_for(int64_t total_rows) {
+  // sentinel key == total_rows marks an invalid id; it must be representable
+  int bits = 1;
+  while (bits < 64 && (uint64_t(1) << bits) <= (uint64_t)total_rows) ++bits;
+  return bits;
+}
+
+// ---------------------------------------------------------------------------
+// 1. key build
+
+template <typename Idx, typename Key>
+__global__ void __launch_bounds__(256)
+build_keys_kernel(int32_t T, int64_t B, const int64_t* __restrict__ row_offsets,
+                  const Idx* __restrict__ indices, const int64_t* __restrict__ offsets,
+                  Key* __restrict__ keys, int32_t* __restrict__ bags, Key sentinel,
+                  neo_error* err) {
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int64_t bag = (int64_t)blockIdx.x * 8 + warp;
+  if (bag >= (int64_t)T * B) return;
+  const int32_t t = (int32_t)(bag / B);
+  const int64_t rbase = row_offsets[t];
+  const int64_t H = row_offsets[t + 1] - rbase;
+  const int64_t base0 = offsets[0];
+  const int64_t start = offsets[bag], end = offsets[bag + 1];
+  for (int64_t p = start + lane; p < end; p += kWarp) {
+    const int64_t v = (int64_t)indices[p];
+    Key k;
+    if (v < 0 || v >= H) {
+      record_bad_index(err, p);
+      k = sentinel;
+    } else {
+      k = (Key)(rbase + v);
+    }
+    keys[p - base0] = k;
+    bags[p - base0] = (int32_t)bag;
+  }
+}
+
+// 3. segment heads
+template <typename Key>
+struct HeadFlag {
+  const Key* keys;
+  __device__ __forceinline__ bool operator()(const int32_t& i) const {
+    return i == 0 || keys[i] != keys[i - 1];
+  }
+};
+
+// ---------------------------------------------------------------------------
+// 4. segment reduce + optimizer
+
+struct SegParams {
+  int32_t T;
+  int64_t B;
+  const int64_t* row_offsets;
+  int64_t total_rows;
+  const int32_t* dim_offsets;
+  int32_t max_dim;
+  const uint64_t* weights;
+  const uint64_t* moments;
+  const void* grad;
+  int64_t grad_stride;
+  int32_t pooling;
+  const int64_t* offsets;  // for MEAN pooling: bag lengths
+  int32_t mode;
+  int32_t optim;
+  double lr;
+  double eps;
+  int64_t* out_ids;
+  void* out_grads;
+  const uint64_t* dense_grads;
+  const void* keys;
+  const int32_t* bags;
+  const int32_t* seg_starts;
+  const int64_t* num_segs;
+  int64_t N;
+};
+
+// aggregate the segment's upstream rows into g (warp-private smem row)
+template <typename G, typename Acc, int VEC>
+__device__ __forceinline__ void aggregate_row(const SegParams& p, const G* __restrict__ grad,
+                                              int32_t t, int32_t D, int32_t doff, int64_t s0,
+                                              int64_t s1, Acc* g, int lane) {
+  constexpr bool kExact = sizeof(Acc) == 8;
+  constexpr int U = kBwdUnroll;
+  const int chunks = D / VEC;
+  const int S = kExact ? kWarp : subwarp_width(chunks);
+  const int R = kWarp / S;
+  const int sub = lane / S, sl = lane % S;
+  const int64_t bag_base = (int64_t)t * p.B;
+  for (int cbase = 0; cbase < chunks; cbase += S) {
+    const int ch = cbase + sl;
+    const bool col_live = ch < chunks;
+    Acc acc[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) acc[e] = Acc(0);
+    for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
+      const int m = (int)min64(kWarp, s1 - j0);
+      const int32_t mybag = lane < m ? p.bags[j0 + lane] : 0;
+      for (int jj = 0; jj < m; jj += R * U) {
+        Vec<G, VEC> v[U];
+        bool live[U];
+        Acc scale[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int r = jj + u * R + sub;
+          const int32_t bg = __shfl_sync(0xffffffffu, mybag, r < m ? r : 0);
+          live[u] = r < m;
+          const int64_t b = (int64_t)bg - bag_base;
+          scale[u] = Acc(1);
+          if (p.pooling == NEO_POOL_MEAN && live[u]) {
+            const int64_t len = p.offsets[bg + 1] - p.offsets[bg];
+            scale[u] = Acc(1) / (Acc)len;
+          }
+          if (live[u] && col_live) {
+            v[u] = ld_vec<G, VEC>(grad + b * p.grad_stride + doff + (int64_t)ch * VEC);
+          } else {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) v[u].v[e] = G(0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (kExact && !live[u]) continue;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) {
+            Acc x = to_acc<Acc>(v[u].v[e]);
+            if (p.pooling == NEO_POOL_MEAN) x = x * scale[u];
+            acc[e] += x;
+          }
+        }
+      }
+    }
+    if (!kExact) {
+      for (int o = S; o < kWarp; o <<= 1) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+      }
+    }
+    if (sub == 0 && col_live) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) g[ch * VEC + e] = acc[e];
+    }
+  }
+  __syncwarp();
+}
+
+template <typename W, typename G, typename Key>
+__global__ void __launch_bounds__(kBwdWarps * kWarp)
+tbe_segment_kernel(SegParams p) {
+  constexpr bool kExact = sizeof(W) == 8;
+  using Acc = typename std::conditional<kExact, double, float>::type;
+  constexpr int kVec = 16 / sizeof(W);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  Acc* g = reinterpret_cast<Acc*>(smem_raw) + (size_t)warp * p.max_dim;
+  const G* grad = reinterpret_cast<const G*>(p.grad);
+  const Key* keys = reinterpret_cast<const Key*>(p.keys);
+  const int64_t U = *p.num_segs;
+  const int64_t nwarps = (int64_t)gridDim.x * kBwdWarps;
+  for (int64_t seg = (int64_t)blockIdx.x * kBwdWarps + warp; seg < U; seg += nwarps) {
+    const int64_t s0 = p.seg_starts[seg];
+    const int64_t s1 = seg + 1 < U ? (int64_t)p.seg_starts[seg + 1] : p.N;
+    const uint64_t key = (uint64_t)keys[s0];
+    if (key >= (uint64_t)p.total_rows) continue;  // invalid ids sort last
+    const int32_t t = (int32_t)(p.bags[s0] / p.B);
+    const int64_t row = (int64_t)key - p.row_offsets[t];
+    const int32_t doff = p.dim_offsets[t];
+    const int32_t D = p.dim_offsets[t + 1] - doff;
+    W* wbase = reinterpret_cast<W*>(p.weights[t]);
+    Acc* mbase = p.moments ? reinterpret_cast<Acc*>(p.moments[t]) : nullptr;
+    RowPrefetch<W, Acc> pf;
+    prefetch_row<W, Acc>(p.mode == NEO_BWD_UPDATE, wbase, mbase, p.optim, row, D, lane, pf);
+    const bool vec = (D % kVec) == 0 && (doff % kVec) == 0 && (p.grad_stride % kVec) == 0 &&
+                     (reinterpret_cast<uintptr_t>(grad) % min(16, (int)sizeof(G) * kVec)) == 0;
+    if (vec) aggregate_row<G, Acc, kVec>(p, grad, t, D, doff, s0, s1, g, lane);
+    else aggregate_row<G, Acc, 1>(p, grad, t, D, doff, s0, s1, g, lane);
+
+    if (p.mode == NEO_BWD_UPDATE) {
+      update_row<W, Acc>(wbase, mbase, p.optim, p.lr, p.eps, row, D, g, lane, pf);
+    } else if (p.mode == NEO_BWD_AGGREGATE) {
+      Acc* og = reinterpret_cast<Acc*>(p.out_grads) + seg * p.max_dim;
+      for (int j = lane; j < D; j += kWarp) og[j] = g[j];
+      if (lane == 0) p.out_ids[seg] = (int64_t)key;
+    } else {  // DENSE
+      Acc* dg = reinterpret_cast<Acc*>(p.dense_grads[t]) + row * D;
+      for (int j = lane; j < D; j += kWarp) dg[j] = g[j];
+    }
+    __syncwarp();
+  }
+}
+
+template <typename Key>
+__global__ void count_valid_kernel(const Key* keys, const int32_t* seg_starts,
+                                   const int64_t* num_segs, int64_t total_rows, int64_t* out) {
+  const int64_t U = *num_segs;
+  int64_t c = U;
+  if (U > 0 && (uint64_t)keys[seg_starts[U - 1]] >= (uint64_t)total_rows) c = U - 1;
+  *out = c;
+}
+
+// ---------------------------------------------------------------------------
+
+template <typename Key>
+static size_t cub_temp_bytes(int64_t N) {
+  size_t sort_bytes = 0, sel_bytes = 0;
+  cub::DoubleBuffer<Key> kb(nullptr, nullptr);
+  cub::DoubleBuffer<int32_t> vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, kb, vb, (int)N, 0, sizeof(Key) * 8);
+  cub::CountingInputIterator<int32_t> it(0);
+  cub::DeviceSelect::If(nullptr, sel_bytes, it, (int32_t*)nullptr, (int64_t*)nullptr, (int)N,
+                        HeadFlag<Key>{nullptr});
+  return sort_bytes > sel_bytes ? sort_bytes : sel_bytes;
+}
+
+template <typename Key>
+static size_t workspace_for(int64_t N) {
+  size_t b = 0;
+  b += 2 * align256(sizeof(Key) * N);      // key double buffer
+  b += 2 * align256(sizeof(int32_t) * N);  // bag double buffer
+  b += align256(sizeof(int32_t) * N);      // segment starts
+  b += align256(sizeof(int64_t) * 2);      // segment count
+  b += align256(cub_temp_bytes<Key>(N));
+  return b;
+}
+
+static bool use_wide_keys(int64_t total_rows) { return total_rows >= (int64_t)UINT32_MAX; }
+
+template <typename W, typename G, typename Key>
+static int launch_segments(const SegParams& p, cudaStream_t s) {
+  using Acc = typename std::conditional<sizeof(W) == 8, double, float>::type;
+  const size_t smem = (size_t)kBwdWarps * p.max_dim * sizeof(Acc);
+  auto kern = tbe_segment_kernel<W, G, Key>;
+  if (smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return fail(NEO_E_ARG, "neo_tbe_backward: max_dim too large for shared memory");
+  }
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwdWarps * kWarp, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t max_blocks = (p.N + kBwdWarps - 1) / kBwdWarps;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > max_blocks) grid = max_blocks;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, kBwdWarps * kWarp, smem, s>>>(p);
+  return check_launch("neo_tbe_backward(segments)");
+}
+
+template <typename Key>
+static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
+                        const void* indices, int32_t index_dtype, void* workspace,
+                        size_t ws_bytes, int64_t* out_count, neo_error* err, cudaStream_t s) {
+  const int64_t N = p.N;
+  if (ws_bytes < workspace_for<Key>(N))
+    return fail(NEO_E_ARG, "neo_tbe_backward: workspace too small");
+  unsigned char* w = static_cast<unsigned char*>(workspace);
+  Key* k0 = reinterpret_cast<Key*>(w);
+  w += align256(sizeof(Key) * N);
+  Key* k1 = reinterpret_cast<Key*>(w);
+  w += align256(sizeof(Key) * N);
+  int32_t* v0 = reinterpret_cast<int32_t*>(w);
+  w += align256(sizeof(int32_t) * N);
+  int32_t* v1 = reinterpret_cast<int32_t*>(w);
+  w += align256(sizeof(int32_t) * N);
+  int32_t* starts = reinterpret_cast<int32_t*>(w);
+  w += align256(sizeof(int32_t) * N);
+  int64_t* nseg = reinterpret_cast<int64_t*>(w);
+  w += align256(sizeof(int64_t) * 2);
+  void* temp = w;
+  size_t temp_bytes = cub_temp_bytes<Key>(N);
+
+  const int64_t bags = (int64_t)p.T * p.B;
+  const unsigned kb_blocks = (unsigned)((bags + 7) / 8);
+  const Key sentinel = (Key)p.total_rows;
+  if (index_dtype == NEO_I32)
+    build_keys_kernel<int32_t, Key><<<kb_blocks, 256, 0, s>>>(
+        p.T, p.B, p.row_offsets, (const int32_t*)indices, p.offsets, k0, v0, sentinel, err);
+  else
+    build_keys_kernel<int64_t, Key><<<kb_blocks, 256, 0, s>>>(
+        p.T, p.B, p.row_offsets, (const int64_t*)indices, p.offsets, k0, v0, sentinel, err);
+  int rc = check_launch("neo_tbe_backward(keys)");
+  if (rc) return rc;
+
+  cub::DoubleBuffer<Key> kbuf(k0, k1);
+  cub::DoubleBuffer<int32_t> vbuf(v0, v1);
+  const int bits = key_bits_for(p.total_rows);
+  if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kbuf, vbuf, (int)N, 0, bits, s) !=
+      cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tbe_backward: radix sort failed");
+  const Key* keys = kbuf.Current();
+  cub::CountingInputIterator<int32_t> it(0);
+  temp_bytes = cub_temp_bytes<Key>(N);
+  if (cub::DeviceSelect::If(temp, temp_bytes, it, starts, nseg, (int)N, HeadFlag<Key>{keys}, s) !=
+      cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tbe_backward: segment select failed");
+  p.keys = keys;
+  p.bags = vbuf.Current();
+  p.seg_starts = starts;
+  p.num_segs = nseg;
+
+  switch (weight_dtype) {
+    case NEO_F64:
+      if (grad_dtype != NEO_F64) return fail(NEO_E_ARG, "F64 tables take F64 gradients");
+      rc = launch_segments<double, double, Key>(p, s);
+      break;
+    case NEO_F32:
+    case NEO_F16: {
+      const bool h = weight_dtype == NEO_F16;
+      switch (grad_dtype) {
+        case NEO_F32:
+          rc = h ? launch_segments<__half, float, Key>(p, s) : launch_segments<float, float, Key>(p, s);
+          break;
+        case NEO_BF16:
+          rc = h ? launch_segments<__half, __nv_bfloat16, Key>(p, s)
+                 : launch_segments<float, __nv_bfloat16, Key>(p, s);
+          break;
+        case NEO_F16:
+          rc = h ? launch_segments<__half, __half, Key>(p, s) : launch_segments<float, __half, Key>(p, s);
+          break;
+        default:
+          return fail(NEO_E_ARG, "neo_tbe_backward: gradient dtype must be F32, BF16 or F16");
+      }
+      break;
+    }
+    default:
+      return fail(NEO_E_ARG, "neo_tbe_backward: weight dtype must be F32, F16 or F64");
+  }
+  if (rc) return rc;
+  if (out_count) {
+    count_valid_kernel<Key><<<1, 1, 0, s>>>(keys, starts, nseg, p.total_rows, out_count);
+    rc = check_launch("neo_tbe_backward(count)");
+    if (rc) return rc;
+  }
+  launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
+  return check_launch("neo_tbe_backward(finalize)");
+}
+
+}  // namespace neo
+
+extern "C" size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows) {
+  if (num_indices < 1) num_indices = 1;
+  return neo::use_wide_keys(total_rows) ? neo::workspace_for<uint64_t>(num_indices)
+                                        : neo::workspace_for<uint32_t>(num_indices);
+}
+
+extern "C" int neo_tbe_backward(int32_t num_tables, int64_t batch, const int64_t* row_offsets,
+                                int64_t total_rows, const int32_t* dim_offsets, int32_t max_dim,
+                                const uint64_t* weights, int32_t weight_dtype,
+                                const uint64_t* moments, const void* indices,
+                                int32_t index_dtype, const int64_t* offsets, int64_t num_indices,
+                                int32_t pooling, const void* grad, int32_t grad_dtype,
+                                int64_t grad_stride, int32_t mode, int32_t optim, double lr,
+                                double eps, int64_t* out_ids, void* out_grads,
+                                int64_t* out_count, const uint64_t* dense_grads, void* workspace,
+                                size_t workspace_bytes, neo_error* err, void* stream) {
+  using namespace neo;
+  cudaStream_t s = as_stream(stream);
+  if (num_tables < 0 || batch < 0 || num_indices < 0 || max_dim < 0 || total_rows < 0)
+    return fail(NEO_E_ARG, "neo_tbe_backward: negative size");
+  if ((int64_t)num_tables * batch >= INT_MAX || num_indices >= INT_MAX)
+    return fail(NEO_E_ARG, "neo_tbe_backward: more than 2^31 bags or indices in one call");
+  if (mode != NEO_BWD_UPDATE && mode != NEO_BWD_AGGREGATE && mode != NEO_BWD_DENSE)
+    return fail(NEO_E_ARG, "neo_tbe_backward: bad mode");
+  if (mode == NEO_BWD_UPDATE) {
+    if (optim != NEO_OPT_SGD && optim != NEO_OPT_ROWWISE_ADAGRAD && optim != NEO_OPT_ADAGRAD)
+      return fail(NEO_E_ARG, "cfg.kind: unknown optimizer");
+    if (!(lr > 0)) return fail(NEO_E_ARG, "lr: must be > 0");
+    if (eps < 0) return fail(NEO_E_ARG, "eps: must be >= 0");
+    if (optim != NEO_OPT_SGD && !moments) return fail(NEO_E_ARG, "moment: state required");
+  }
+  if (mode == NEO_BWD_AGGREGATE && (!out_ids || !out_grads))
+    return fail(NEO_E_ARG, "neo_tbe_backward: AGGREGATE needs out_ids/out_grads");
+  if (mode == NEO_BWD_DENSE && !dense_grads)
+    return fail(NEO_E_ARG, "neo_tbe_backward: DENSE needs dense_grads");
+  if (pooling != NEO_POOL_SUM && pooling != NEO_POOL_MEAN)
+    return fail(NEO_E_ARG, "neo_tbe_backward: pooling must be SUM or MEAN");
+  if (num_tables == 0 || batch == 0 || num_indices == 0) {
+    if (out_count) {
+      if (cudaMemsetAsync(out_count, 0, sizeof(int64_t), s) != cudaSuccess)
+        return fail(NEO_E_CUDA, "neo_tbe_backward: memset failed");
+    }
+    return NEO_OK;
+  }
+  SegParams p{};
+  p.T = num_tables;
+  p.B = batch;
+  p.row_offsets = row_offsets;
+  p.total_rows = total_rows;
+  p.dim_offsets = dim_offsets;
+  p.max_dim = max_dim;
+  p.weights = weights;
+  p.moments = moments;
+  p.grad = grad;
+  p.grad_stride = grad_stride;
+  p.pooling = pooling;
+  p.offsets = offsets;
+  p.mode = mode;
+  p.optim = optim;
+  p.lr = lr;
+  p.eps = eps;
+  p.out_ids = out_ids;
+  p.out_grads = out_grads;
+  p.dense_grads = dense_grads;
+  p.N = num_indices;
+  if (use_wide_keys(total_rows))
+    return run_backward<uint64_t>(p, weight_dtype, grad_dtype, indices, index_dtype, workspace,
+                                  workspace_bytes, out_count, err, s);
+  return run_backward<uint32_t>(p, weight_dtype, grad_dtype, indices, index_dtype, workspace,
+                                workspace_bytes, out_count, err, s);
+}

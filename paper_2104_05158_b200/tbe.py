@@ -1,0 +1,341 @@
+"""Device-side operator layer: torch tensors in HBM -> libneob200 C ABI.
+
+``TableGroup`` is the production embedding-bag operator: T tables resident
+in HBM (one contiguous weight buffer, per-table views), their optimizer
+state, and the device metadata one TBE launch needs.  Its forward is one
+``neo_tbe_forward`` launch for all tables; its backward is the fused
+sort / segment-reduce / optimizer sequence of ``neo_tbe_backward``.
+
+The free functions wrap the layout kernels (bucketize, permute, offsets,
+piece copies, block gathers, casts).  All calls are stream-ordered on the
+current torch stream and never synchronise, except ``ErrorRecord.read``.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _capi as capi
+from .errors import IndexOutOfRange, InvalidValue
+
+DTYPE_CODE = {
+    torch.float32: capi.NEO_F32,
+    torch.float16: capi.NEO_F16,
+    torch.float64: capi.NEO_F64,
+    torch.bfloat16: capi.NEO_BF16,
+}
+INDEX_CODE = {torch.int32: capi.NEO_I32, torch.int64: capi.NEO_I64}
+OPTIM_CODE = {"sgd": capi.NEO_OPT_SGD, "rowwise_adagrad": capi.NEO_OPT_ROWWISE_ADAGRAD,
+              "adagrad": capi.NEO_OPT_ADAGRAD}
+POOL_CODE = {"sum": capi.NEO_POOL_SUM, "mean": capi.NEO_POOL_MEAN}
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def acc_dtype(weight_dtype: torch.dtype) -> torch.dtype:
+    """Accumulator / optimizer-state type: f64 for f64 tables, else f32."""
+    return torch.float64 if weight_dtype == torch.float64 else torch.float32
+
+
+class _Workspace:
+    """Grow-only per-device scratch buffers (one per purpose)."""
+
+    def __init__(self):
+        self._bufs: dict = {}
+
+    def get(self, key: str, nbytes: int, device) -> torch.Tensor:
+        nbytes = max(int(nbytes), 256)
+        k = (key, str(device))
+        b = self._bufs.get(k)
+        if b is None or b.numel() < nbytes:
+            b = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self._bufs[k] = b
+        return b
+
+
+WORKSPACE = _Workspace()
+
+
+class ErrorRecord:
+    """Device-side neo_error (first bad index in buffer order)."""
+
+    def __init__(self, device):
+        self.buf = torch.empty(3, dtype=torch.int64, device=device)
+
+    def reset(self) -> "ErrorRecord":
+        capi.check(capi.lib().neo_error_reset(self.buf.data_ptr(), _stream()), "neo_error_reset")
+        return self
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+    def read(self):
+        """(position, value, table) of the first bad index, or None (syncs)."""
+        h = self.buf.cpu().numpy()
+        if int(h[0]) == np.iinfo(np.int64).max:
+            return None
+        table = int(np.int32(h[2] & 0xFFFFFFFF))
+        return int(h[0]), int(h[1]), table
+
+
+def _u64_ptrs(tensors, device) -> torch.Tensor:
+    return torch.tensor([0 if t is None else t.data_ptr() for t in tensors], dtype=torch.int64,
+                        device=device)
+
+
+class TableGroup:
+    """T embedding tables sharing one TBE launch.
+
+    rows/dims: per-table H_t, D_t.  weights: optional existing (H_t, D_t)
+    tensors (e.g. shards); otherwise one contiguous HBM buffer is allocated
+    and each table is a view into it.  optim: "sgd" | "rowwise_adagrad" |
+    "adagrad" | None — determines the moment state allocated.
+    """
+
+    def __init__(self, rows: Sequence[int], dims: Sequence[int], dtype=torch.float32,
+                 optim: Optional[str] = "rowwise_adagrad", device="cuda",
+                 weights: Optional[Sequence[torch.Tensor]] = None,
+                 moments: Optional[Sequence[Optional[torch.Tensor]]] = None,
+                 table_ids: Optional[Sequence[str]] = None):
+        if dtype not in (torch.float32, torch.float16, torch.float64):
+            raise InvalidValue("dtype", "tables are stored as f32, f16 or f64")
+        self.rows = [int(r) for r in rows]
+        self.dims = [int(d) for d in dims]
+        self.T = len(self.rows)
+        self.dtype = dtype
+        self.acc = acc_dtype(dtype)
+        self.device = torch.device(device)
+        self.optim = optim
+        self.table_ids = list(table_ids) if table_ids is not None else [str(i) for i in range(self.T)]
+        if weights is None:
+            total = sum(r * d for r, d in zip(self.rows, self.dims))
+            self._storage = torch.empty(total, dtype=dtype, device=self.device)
+            self.weights, off = [], 0
+            for r, d in zip(self.rows, self.dims):
+                self.weights.append(self._storage[off:off + r * d].view(r, d))
+                off += r * d
+        else:
+            self.weights = list(weights)
+            for w, r, d in zip(self.weights, self.rows, self.dims):
+                if w is None:  # gradient-only group (AGGREGATE / DENSE modes)
+                    continue
+                if tuple(w.shape) != (r, d) or w.dtype != dtype or not w.is_contiguous():
+                    raise InvalidValue("weights", "must be contiguous (H, D) tensors of the group dtype")
+        if moments is not None:
+            self.moments = list(moments)
+        elif optim in ("rowwise_adagrad", "adagrad"):
+            self.moments = [
+                torch.zeros(r if optim == "rowwise_adagrad" else (r, d), dtype=self.acc, device=self.device)
+                for r, d in zip(self.rows, self.dims)
+            ]
+        else:
+            self.moments = [None] * self.T
+        self.row_offsets_h = np.concatenate(([0], np.cumsum(self.rows))).astype(np.int64)
+        self.dim_offsets_h = np.concatenate(([0], np.cumsum(self.dims))).astype(np.int32)
+        self.total_rows = int(self.row_offsets_h[-1])
+        self.total_dim = int(self.dim_offsets_h[-1])
+        self.max_dim = max(self.dims) if self.dims else 0
+        self.row_offsets = torch.from_numpy(self.row_offsets_h).to(self.device)
+        self.dim_offsets = torch.from_numpy(self.dim_offsets_h).to(self.device)
+        self.weight_ptrs = _u64_ptrs(self.weights, self.device)
+        self.moment_ptrs = _u64_ptrs(self.moments, self.device)
+
+    # ------------------------------------------------------------------
+    def forward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, pooling: str = "sum",
+                out: Optional[torch.Tensor] = None, out_dtype: Optional[torch.dtype] = None,
+                err: Optional[ErrorRecord] = None) -> torch.Tensor:
+        """Pooled (batch, sum D) output; offsets has T*batch+1 entries."""
+        if out is None:
+            od = out_dtype or (torch.float64 if self.dtype == torch.float64 else torch.float32)
+            out = torch.empty((batch, self.total_dim), dtype=od, device=self.device)
+        stride = out.stride(0) if out.dim() == 2 else self.total_dim
+        rc = capi.lib().neo_tbe_forward(
+            self.T, batch, self.row_offsets.data_ptr(), self.dim_offsets.data_ptr(), self.max_dim,
+            self.weight_ptrs.data_ptr(), DTYPE_CODE[self.dtype], indices.data_ptr(),
+            INDEX_CODE[indices.dtype], offsets.data_ptr(), POOL_CODE[pooling], out.data_ptr(),
+            DTYPE_CODE[out.dtype], stride, err.ptr if err else None, _stream())
+        capi.check(rc, "neo_tbe_forward")
+        return out
+
+    def backward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, grad: torch.Tensor,
+                 mode: str = "update", optim: Optional[str] = None, lr: float = 0.0,
+                 eps: float = 0.0, pooling: str = "sum", err: Optional[ErrorRecord] = None,
+                 dense_grads: Optional[Sequence[torch.Tensor]] = None):
+        """mode "update": fused aggregate + one optimizer step per touched row
+        (in place); "aggregate": returns (ids, grads, count) with global row
+        keys; "dense": accumulates into dense_grads (per table, pre-zeroed)."""
+        n_idx = int(indices.numel())
+        ws_bytes = capi.lib().neo_tbe_backward_workspace_bytes(n_idx, self.total_rows)
+        ws = WORKSPACE.get("tbe_bwd", ws_bytes, self.device)
+        out_ids = out_grads = out_count = None
+        dense_ptrs = None
+        mode_code = {"update": capi.NEO_BWD_UPDATE, "aggregate": capi.NEO_BWD_AGGREGATE,
+                     "dense": capi.NEO_BWD_DENSE}[mode]
+        if mode == "aggregate":
+            out_ids = torch.empty(max(n_idx, 1), dtype=torch.int64, device=self.device)
+            out_grads = torch.empty((max(n_idx, 1), max(self.max_dim, 1)), dtype=self.acc, device=self.device)
+            out_count = torch.zeros(1, dtype=torch.int64, device=self.device)
+        if mode == "dense":
+            dense_ptrs = _u64_ptrs(dense_grads, self.device)
+        optim = optim or self.optim or "sgd"
+        stride = grad.stride(0) if grad.dim() == 2 else self.total_dim
+        rc = capi.lib().neo_tbe_backward(
+            self.T, batch, self.row_offsets.data_ptr(), self.total_rows, self.dim_offsets.data_ptr(),
+            self.max_dim, self.weight_ptrs.data_ptr(), DTYPE_CODE[self.dtype],
+            self.moment_ptrs.data_ptr(), indices.data_ptr(), INDEX_CODE[indices.dtype],
+            offsets.data_ptr(), n_idx, POOL_CODE[pooling], grad.data_ptr(), DTYPE_CODE[grad.dtype],
+            stride, mode_code, OPTIM_CODE[optim], float(lr), float(eps), _ptr(out_ids),
+            _ptr(out_grads), _ptr(out_count), _ptr(dense_ptrs), ws.data_ptr(), ws.numel(),
+            err.ptr if err else None, _stream())
+        capi.check(rc, "neo_tbe_backward")
+        if mode == "aggregate":
+            return out_ids, out_grads, out_count
+        return None
+
+
+# ---------------------------------------------------------------------------
+# layout kernels
+
+
+def lengths_to_offsets(lengths: torch.Tensor) -> torch.Tensor:
+    """int64 offsets (n+1) of int64 lengths (model.py:365-370), on device."""
+    n = int(lengths.numel())
+    out = torch.empty(n + 1, dtype=torch.int64, device=lengths.device)
+    ws_bytes = capi.lib().neo_scan_workspace_bytes(n)
+    ws = WORKSPACE.get("scan", ws_bytes, lengths.device)
+    capi.check(capi.lib().neo_lengths_to_offsets(n, lengths.data_ptr(), out.data_ptr(), ws.data_ptr(),
+                                                 ws.numel(), _stream()), "neo_lengths_to_offsets")
+    return out
+
+
+def bucketize_rowwise(offsets: torch.Tensor, indices: torch.Tensor, starts: Sequence[int],
+                      err: Optional[ErrorRecord] = None):
+    """Row-wise bucketisation (comms.py:107-141) of n bags.
+
+    starts: k+1 shard boundaries (host ints).  Returns (lengths (k, n),
+    offsets (k*n+1), indices) with shard s's ids at
+    indices[offsets[s*n]:offsets[(s+1)*n]], rebased to the shard."""
+    n = int(offsets.numel()) - 1
+    k = len(starts) - 1
+    dev = indices.device
+    out_len = torch.empty((k, n), dtype=torch.int64, device=dev)
+    out_off = torch.empty(k * n + 1, dtype=torch.int64, device=dev)
+    out_idx = torch.empty_like(indices)
+    ws_bytes = capi.lib().neo_bucketize_workspace_bytes(n, k)
+    ws = WORKSPACE.get("bucketize", ws_bytes, dev)
+    starts_arr = np.asarray(starts, dtype=np.int64)
+    st = starts_arr.ctypes.data_as(capi.C.POINTER(capi.C.c_int64))
+    capi.check(capi.lib().neo_bucketize_rowwise(
+        n, offsets.data_ptr(), indices.data_ptr(), INDEX_CODE[indices.dtype], k, st,
+        out_len.data_ptr(), out_off.data_ptr(), out_idx.data_ptr(), -1,
+        err.ptr if err else None, ws.data_ptr(), ws.numel(), _stream()), "neo_bucketize_rowwise")
+    return out_len, out_off, out_idx
+
+
+def permute_blocks(outer: int, inner: int, B: int, lengths: torch.Tensor, indices: torch.Tensor):
+    """(outer, inner, B) block order -> (inner, outer, B) (comms.py:222-257)."""
+    dev = lengths.device
+    out_len = torch.empty_like(lengths)
+    out_idx = torch.empty_like(indices)
+    ws_bytes = capi.lib().neo_permute_workspace_bytes(outer, inner)
+    ws = WORKSPACE.get("permute", ws_bytes, dev)
+    capi.check(capi.lib().neo_permute_blocks(
+        outer, inner, B, lengths.data_ptr(), indices.data_ptr(), INDEX_CODE[indices.dtype],
+        out_len.data_ptr(), out_idx.data_ptr(), ws.data_ptr(), ws.numel(), _stream()),
+        "neo_permute_blocks")
+    return out_len, out_idx
+
+
+@dataclass
+class Piece:
+    """One column block copy src[:, src_col:src_col+width] -> dst[:, dst_col:...]."""
+
+    src: torch.Tensor
+    dst: torch.Tensor
+    src_col: int
+    dst_col: int
+    width: int
+    accumulate: bool = False
+
+
+def copy_pieces(rows: int, pieces: Sequence[Piece], pieces_dev: Optional[torch.Tensor] = None) -> None:
+    """Apply pieces in order to rows [0, rows) (neo_copy_pieces)."""
+    if not pieces:
+        return
+    sd, dd = pieces[0].src.dtype, pieces[0].dst.dtype
+    if pieces_dev is None:
+        pieces_dev = pack_pieces(pieces, pieces[0].src.device)
+    capi.check(capi.lib().neo_copy_pieces(rows, pieces_dev.data_ptr(), len(pieces), DTYPE_CODE[sd],
+                                          DTYPE_CODE[dd], _stream()), "neo_copy_pieces")
+
+
+def pack_pieces(pieces: Sequence[Piece], device) -> torch.Tensor:
+    arr = (capi.NeoPiece * len(pieces))()
+    for i, p in enumerate(pieces):
+        arr[i] = capi.NeoPiece(p.src.data_ptr(), p.dst.data_ptr(), p.src.stride(0), p.dst.stride(0),
+                               p.src_col, p.dst_col, p.width, int(p.accumulate))
+    raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+    return torch.from_numpy(raw).to(device)
+
+
+def gather_blocks(srcs: Sequence[torch.Tensor], counts: Sequence[int], dst: torch.Tensor) -> torch.Tensor:
+    """Concatenate the first counts[i] elements of each srcs[i] into dst
+    (one launch; dst element size 4 or 8)."""
+    n = len(srcs)
+    if n == 0:
+        return dst
+    offs = np.concatenate(([0], np.cumsum(counts)[:-1])).astype(np.int64)
+    meta = torch.tensor(np.stack([np.array([s.data_ptr() for s in srcs], dtype=np.int64),
+                                  np.asarray(counts, dtype=np.int64), offs]),
+                        dtype=torch.int64).to(dst.device)
+    capi.check(capi.lib().neo_gather_blocks(n, meta[0].data_ptr(), meta[1].data_ptr(), meta[2].data_ptr(),
+                                            dst.data_ptr(), dst.element_size(), _stream()),
+               "neo_gather_blocks")
+    return dst
+
+
+def cast(x: torch.Tensor, dtype: torch.dtype, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """RNE element-wise conversion on device (neo_cast)."""
+    out = torch.empty(x.shape, dtype=dtype, device=x.device) if out is None else out
+    capi.check(capi.lib().neo_cast(x.numel(), x.data_ptr(), DTYPE_CODE[x.dtype], out.data_ptr(),
+                                   DTYPE_CODE[dtype], _stream()), "neo_cast")
+    return out
+
+
+def fp16_roundtrip_(x: torch.Tensor):
+    """In-place f64 -> binary16 (RNE) -> f64; returns (overflow mask, nonfinite flag) device tensors."""
+    assert x.dtype == torch.float64 and x.is_contiguous()
+    ovf = torch.zeros(x.shape, dtype=torch.uint8, device=x.device)
+    nonfinite = torch.zeros(1, dtype=torch.int32, device=x.device)
+    capi.check(capi.lib().neo_fp16_roundtrip(x.numel(), x.data_ptr(), ovf.data_ptr(), nonfinite.data_ptr(),
+                                             _stream()), "neo_fp16_roundtrip")
+    return ovf, nonfinite
+
+
+def apply_row_updates(weight: torch.Tensor, moment: Optional[torch.Tensor], ids: Optional[torch.Tensor],
+                      grads: torch.Tensor, optim: str, lr: float, eps: float) -> None:
+    """One optimizer step per listed row (embedding.py:212-267)."""
+    n = int(grads.shape[0])
+    capi.check(capi.lib().neo_apply_row_updates(
+        n, _ptr(ids), grads.data_ptr(), int(weight.shape[1]), weight.data_ptr(),
+        DTYPE_CODE[weight.dtype], _ptr(moment), OPTIM_CODE[optim], float(lr), float(eps), _stream()),
+        "neo_apply_row_updates")
+
+
+def raise_if_bad(err: ErrorRecord, table_ids: Sequence[str]) -> None:
+    """Raise the reference's IndexOutOfRange for the first bad id (syncs)."""
+    r = err.read()
+    if r is not None:
+        _, value, table = r
+        tid = table_ids[table] if 0 <= table < len(table_ids) else ""
+        raise IndexOutOfRange(tid, value)

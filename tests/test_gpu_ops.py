@@ -1,0 +1,270 @@
+"""GPU parity of the TBE operators against the reference's fixtures and the
+CPU oracle.  f64 instantiations must be BIT-EXACT (they reproduce numpy's
+order); f32/f16 production instantiations must sit within the stated
+tolerance: |got - ref| <= 1e-5 * sum_i |term_i| (+ one storage ulp) for pooled
+outputs, rtol 1e-5 on |w| + |dw| for updated weights and moments."""
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tbe_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FWD_RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_2104_05158_b200 as p
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    p.load()  # loads libneob200.so; raises if it is missing (no fallback)
+    return p
+
+
+def _table(pkg, values, moment=None, tid="t"):
+    spec = pkg.TableSpec(id=tid, num_rows=values.shape[0], dim=values.shape[1], avg_pooling=1.0)
+    return pkg.EmbeddingTable(spec, values.copy(), None if moment is None else moment.copy())
+
+
+# ---------------------------------------------------------------------------
+# f64: bit-exact with the reference
+
+
+def test_forward_pooled_bitwise(pkg, ops_golden):
+    z = ops_golden
+    for i in range(int(z["ndims"])):
+        t = _table(pkg, z[f"fwd{i}_values"])
+        got = pkg.forward_pooled(t, z[f"fwd{i}_lengths"], z[f"fwd{i}_indices"])
+        assert np.array_equal(got, z[f"fwd{i}_out"]), i
+
+
+def test_forward_hand_vectors_and_errors(pkg):
+    v = np.array([[1.0, 2.0], [3.0, 4.0], [5.0, 6.0]])
+    assert pkg.forward_pooled(_table(pkg, v), [2], [0, 2]).tolist() == [[6, 8]]
+    assert pkg.forward_pooled(_table(pkg, v[:2]), [0, 1], [0]).tolist() == [[0, 0], [1, 2]]
+    with pytest.raises(pkg.IndexOutOfRange) as e:
+        pkg.forward_pooled(_table(pkg, v, tid="zz"), [2, 2], [0, 7, 1, 9])
+    assert e.value.index == 7 and e.value.table_id == "zz"
+    with pytest.raises(pkg.LayoutMismatch):
+        pkg.forward_pooled(_table(pkg, v), [3], [0, 1])
+
+
+def test_backward_aggregate_bitwise(pkg, ops_golden):
+    z = ops_golden
+    for i in range(int(z["ndims"])):
+        g = pkg.backward_sort_aggregate(z[f"fwd{i}_lengths"], z[f"fwd{i}_indices"], z[f"bwd{i}_upstream"])
+        assert np.array_equal(g.ids, z[f"bwd{i}_ids"]), i
+        assert np.array_equal(g.grads, z[f"bwd{i}_grads"]), i
+    g = pkg.backward_sort_aggregate([3], [9, -2, 5], np.ones((1, 2)))  # np.unique semantics
+    assert g.ids.tolist() == [-2, 5, 9]
+
+
+def test_fused_backward_update_bitwise(pkg, ops_golden):
+    z = ops_golden
+    for i in range(int(z["ndims"])):
+        for kind in ("sgd", "rowwise_adagrad", "adagrad"):
+            m0 = z[f"upd{i}_{kind}_m0"]
+            t = _table(pkg, z[f"fwd{i}_values"], None if m0.size == 0 else m0)
+            cfg = pkg.OptimizerConfig(pkg.OptimizerKind(kind), lr=0.05, eps=1e-8)
+            pkg.fused_backward_update(t, z[f"fwd{i}_lengths"], z[f"fwd{i}_indices"], z[f"bwd{i}_upstream"], cfg)
+            assert np.array_equal(t.values, z[f"upd{i}_{kind}_values"]), (i, kind)
+            if m0.size:
+                assert np.array_equal(t.moment, z[f"upd{i}_{kind}_moment"]), (i, kind)
+
+
+def test_apply_optimizer_from_rowgradients_bitwise(pkg, ops_golden):
+    z = ops_golden
+    for i in range(int(z["ndims"])):
+        grads = pkg.RowGradients(z[f"bwd{i}_ids"], z[f"bwd{i}_grads"])
+        for kind in ("sgd", "rowwise_adagrad", "adagrad"):
+            m0 = z[f"upd{i}_{kind}_m0"]
+            t = _table(pkg, z[f"fwd{i}_values"], None if m0.size == 0 else m0)
+            pkg.apply_optimizer(t, grads, pkg.OptimizerConfig(pkg.OptimizerKind(kind), lr=0.05, eps=1e-8))
+            assert np.array_equal(t.values, z[f"upd{i}_{kind}_values"]), (i, kind)
+
+
+def test_rowwise_hand_vector(pkg):  # test_embedding.py:220-231
+    t = _table(pkg, np.array([[1.0, 1.0]]), np.zeros(1))
+    cfg = pkg.OptimizerConfig(pkg.OptimizerKind.ROWWISE_ADAGRAD, lr=0.1, eps=0.0)
+    pkg.apply_rowwise_adagrad(t, pkg.RowGradients(np.array([0]), np.array([[3.0, 4.0]])), cfg)
+    assert t.moment[0] == 12.5
+    t2 = _table(pkg, np.array([[1.0, 1.0]]), np.array([4.0]))
+    pkg.apply_rowwise_adagrad(t2, pkg.RowGradients(np.array([0]), np.array([[0.0, 0.0]])), cfg)
+    assert t2.values.tolist() == [[1.0, 1.0]] and t2.moment.tolist() == [4.0]
+
+
+def test_fp16_roundtrip_bitwise(pkg, ops_golden):
+    q, ovf = pkg.quantize_fp16_roundtrip(ops_golden["fp16_x"])
+    assert np.array_equal(q, ops_golden["fp16_q"]) and np.array_equal(ovf, ops_golden["fp16_ovf"])
+    with pytest.raises(pkg.InvalidValue):
+        pkg.quantize_fp16_roundtrip(np.array([np.inf]))
+
+
+def test_bucketize_and_permute_bit_exact(pkg, ops_golden):
+    z = ops_golden
+    for i in range(8):
+        st = z[f"bkt{i}_starts"]
+        bounds = list(zip(st[:-1].tolist(), st[1:].tolist()))
+        parts = pkg.bucketize_rowwise(z[f"bkt{i}_lengths"], z[f"bkt{i}_indices"], bounds)
+        assert np.array_equal(np.stack([p[0] for p in parts]), z[f"bkt{i}_out_lengths"])
+        assert np.array_equal(np.concatenate([p[1] for p in parts]), z[f"bkt{i}_out_indices"])
+    with pytest.raises(pkg.IndexOutOfRange):
+        pkg.bucketize_rowwise([1], [10], [(0, 5), (5, 10)])
+    with pytest.raises(pkg.InvalidValue):
+        pkg.bucketize_rowwise([1], [1], [(0, 5), (6, 10)])
+    for i in range(6):
+        W, T, B = (int(v) for v in z[f"perm{i}_wtb"])
+        laid = pkg.LaidOutBatch(pkg.GlobalBatchLayout(W, T, B, pkg.LayoutTag.WTB),
+                                z[f"perm{i}_lengths"], z[f"perm{i}_indices"])
+        out = pkg.permute_WTB_to_TWB(laid)
+        assert np.array_equal(out.lengths, z[f"perm{i}_out_lengths"])
+        assert np.array_equal(out.indices, z[f"perm{i}_out_indices"])
+        back = pkg.permute_TWB_to_WTB(out)
+        assert np.array_equal(back.indices, z[f"perm{i}_indices"])
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def test_train_step_reference_config1_bitwise(pkg, c1_digest):
+    """Full config 1 through the GPU f64 path: bit-identical to the reference."""
+    tables = [pkg.TableSpec(id=f"t{i}", num_rows=100_000, dim=64, avg_pooling=20.0) for i in range(8)]
+    model = pkg.ModelSpec(tables=tuple(tables), local_batch=2048)
+    cfg = pkg.OptimizerConfig(pkg.OptimizerKind.ROWWISE_ADAGRAD, lr=0.05, eps=1e-8)
+    batch = pkg.gen_synthetic_batch(model, 2048, seed=0)
+    out, tabs = pkg.train_step_reference(model, batch, cfg, seed=0)
+    assert _sha(out) == c1_digest["out"]
+    assert [_sha(t.values) for t in tabs] == c1_digest["values"]
+    assert [_sha(t.moment) for t in tabs] == c1_digest["moment"]
+
+
+def test_train_step_reference_fixtures_bitwise(pkg, steps_golden):
+    z, plans = steps_golden
+    for c, meta in plans.items():
+        tables = [pkg.TableSpec(id=d["id"], num_rows=d["num_rows"], dim=d["dim"], avg_pooling=d["avg_pooling"],
+                                value_precision=pkg.Precision(d["value_precision"])) for d in meta["tables"]]
+        model = pkg.ModelSpec(tables=tuple(tables), local_batch=meta["local_batch"])
+        batch = pkg.CombinedBatch(z[f"s{c}_lengths"], z[f"s{c}_indices"])
+        cfg = pkg.OptimizerConfig(pkg.OptimizerKind(meta["kind"]), lr=meta["lr"], eps=meta["eps"])
+        out, tabs = pkg.train_step_reference(model, batch, cfg, seed=meta["seed"])
+        assert np.array_equal(out, z[f"s{c}_ref_out"]), c
+        for t, tab in enumerate(tabs):
+            assert np.array_equal(tab.values, z[f"s{c}_ref_t{t}"]), (c, t)
+
+
+# ---------------------------------------------------------------------------
+# f32 / f16 production path: tolerance vs the f64 oracle
+
+
+def _random_group_case(rng, T, rows, dims, B, Lmax):
+    lengths = rng.integers(0, Lmax + 1, size=(T, B))
+    idx = np.concatenate([rng.integers(0, rows[t], size=int(lengths[t].sum())) for t in range(T)])
+    return lengths, idx
+
+
+@pytest.mark.parametrize("wdtype", [torch.float32, torch.float16])
+@pytest.mark.parametrize("idtype", [torch.int32, torch.int64])
+def test_group_forward_f32_tolerance(pkg, wdtype, idtype):
+    from paper_2104_05158_b200 import tbe
+
+    rng = np.random.default_rng(7)
+    dims = [32, 64, 128, 256, 8, 24, 100]
+    rows = [int(r) for r in rng.integers(1000, 20000, size=len(dims))]
+    B = 513
+    lengths, idx = _random_group_case(rng, len(dims), rows, dims, B, 40)
+    grp = tbe.TableGroup(rows, dims, dtype=wdtype, optim=None)
+    for w in grp.weights:
+        w.copy_(torch.randn(w.shape, device="cuda").to(wdtype))
+    off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+    out = grp.forward(torch.from_numpy(idx).to(idtype).cuda(), off, B).cpu().numpy()
+    tab_off = O.offsets_of(lengths.sum(axis=1))
+    col = 0
+    for t, D in enumerate(dims):
+        v = grp.weights[t].double().cpu().numpy()
+        part = idx[tab_off[t]:tab_off[t + 1]]
+        want = O.forward_pooled_c(v, lengths[t], part)
+        bound = O.forward_pooled_c(np.abs(v), lengths[t], part)
+        err = np.abs(out[:, col:col + D] - want)
+        assert (err <= FWD_RTOL * bound + 1e-30).all(), (t, D, err.max())
+        col += D
+
+
+@pytest.mark.parametrize("kind", ["rowwise_adagrad", "adagrad", "sgd"])
+@pytest.mark.parametrize("gdtype", [torch.float32, torch.bfloat16])
+def test_group_backward_update_f32_tolerance(pkg, kind, gdtype):
+    from paper_2104_05158_b200 import tbe
+
+    rng = np.random.default_rng(11)
+    dims = [64, 128, 32, 256]
+    rows = [3000, 5000, 800, 2000]
+    B = 1024
+    lengths, idx = _random_group_case(rng, len(dims), rows, dims, B, 24)
+    grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim=kind)
+    for w in grp.weights:
+        w.copy_(torch.randn(w.shape, device="cuda"))
+    w0 = [w.double().cpu().numpy() for w in grp.weights]
+    grad = torch.randn((B, grp.total_dim), device="cuda").to(gdtype)
+    off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+    lr, eps = 0.05, 1e-8
+    grp.backward(torch.from_numpy(idx).int().cuda(), off, B, grad, mode="update", optim=kind, lr=lr, eps=eps)
+    up = grad.double().cpu().numpy()
+    tab_off = O.offsets_of(lengths.sum(axis=1))
+    col = 0
+    for t, D in enumerate(dims):
+        v = w0[t].copy()
+        m = None if kind == "sgd" else (np.zeros(rows[t]) if kind == "rowwise_adagrad" else np.zeros((rows[t], D)))
+        ids, g = O.backward_aggregate_c(lengths[t], idx[tab_off[t]:tab_off[t + 1]], np.ascontiguousarray(up[:, col:col + D]))
+        O.apply_c(kind, v, m, ids, g, lr, eps)
+        got = grp.weights[t].double().cpu().numpy()
+        tol = 1e-5 * (np.abs(v) + np.abs(v - w0[t])) + 1e-7
+        assert (np.abs(got - v) <= tol).all(), (kind, t, np.abs(got - v).max())
+        if m is not None:
+            gm = grp.moments[t].double().cpu().numpy()
+            assert np.allclose(gm, m, rtol=1e-5, atol=1e-7), (kind, t)
+        col += D
+
+
+def test_group_step_deterministic(pkg):
+    from paper_2104_05158_b200 import tbe
+
+    rng = np.random.default_rng(3)
+    rows, dims, B = [50000] * 4, [128] * 4, 4096
+    lengths, idx = _random_group_case(rng, 4, rows, dims, B, 32)
+    res = []
+    for _ in range(2):
+        torch.manual_seed(0)
+        grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim="rowwise_adagrad")
+        for w in grp.weights:
+            w.copy_(torch.randn(w.shape, device="cuda"))
+        off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+        ix = torch.from_numpy(idx).int().cuda()
+        out = grp.forward(ix, off, B)
+        grp.backward(ix, off, B, torch.ones_like(out), mode="update", optim="rowwise_adagrad", lr=0.05, eps=1e-8)
+        res.append((out.cpu(), grp._storage.cpu(), grp.moments[0].cpu()))
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+    assert torch.equal(res[0][2], res[1][2])
+
+
+def test_mean_pooling_and_fp16_output(pkg):
+    from paper_2104_05158_b200 import tbe
+
+    rng = np.random.default_rng(5)
+    rows, dims, B = [700, 900], [64, 128], 300
+    lengths, idx = _random_group_case(rng, 2, rows, dims, B, 10)
+    grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim=None)
+    for w in grp.weights:
+        w.copy_(torch.randn(w.shape, device="cuda"))
+    off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+    ix = torch.from_numpy(idx).cuda()
+    s = grp.forward(ix, off, B).double().cpu().numpy()
+    m = grp.forward(ix, off, B, pooling="mean").double().cpu().numpy()
+    h = grp.forward(ix, off, B, out_dtype=torch.float16).double().cpu().numpy()
+    L = np.concatenate([np.repeat(lengths[t][:, None], d, axis=1) for t, d in enumerate(dims)], axis=1)
+    want_mean = np.where(L > 0, s / np.maximum(L, 1), 0.0)
+    assert np.allclose(m, want_mean, rtol=1e-6, atol=1e-6)
+    assert np.array_equal(h, O.fp16_roundtrip(s.astype(np.float32))[0])
