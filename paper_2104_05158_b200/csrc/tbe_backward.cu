@@ -231,6 +231,233 @@ tbe_segment_kernel(SegParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// 4'. fast path: chunked segment walk (f32/f16 tables, rows of <= 32 vectors,
+// SUM pooling, UPDATE mode).  Each warp owns a chunk of 32 consecutive sorted
+// (key, bag) entries and processes every segment that STARTS in it (walking
+// past the chunk end for the last one), so segment boundaries come from one
+// coalesced key load + a shuffle instead of a compaction pass, and the weight
+// row / moment of the next segment is prefetched while the current segment's
+// upstream rows are gathered.  Accumulation stays in sorted (= buffer) order.
+
+template <typename W, typename Acc>
+struct SegState {
+  int64_t row;
+  W* w;       // row pointer
+  Acc* m;     // row-wise: &moment[row]; element-wise: moment row
+  int32_t t, D, doff;
+  bool vec, live;
+  W wv[16 / sizeof(W)];
+  Acc mv[16 / sizeof(W)];
+  Acc mr;
+};
+
+template <typename W, typename G, typename Key>
+__device__ __forceinline__ void load_seg_state(const SegParams& p, uint64_t key, int32_t bag, int lane,
+                                               SegState<W, float>& st) {
+  constexpr int kVec = 16 / sizeof(W);
+  st.live = key < (uint64_t)p.total_rows;
+  if (!st.live) return;
+  st.t = bag / (int32_t)p.B;
+  st.row = (int64_t)key - p.row_offsets[st.t];
+  st.doff = p.dim_offsets[st.t];
+  st.D = p.dim_offsets[st.t + 1] - st.doff;
+  W* wbase = reinterpret_cast<W*>(p.weights[st.t]);
+  st.w = wbase + st.row * st.D;
+  const G* grad = reinterpret_cast<const G*>(p.grad);
+  st.vec = (st.D % kVec) == 0 && aligned16(wbase) && (st.doff % kVec) == 0 &&
+           (p.grad_stride % kVec) == 0 &&
+           (reinterpret_cast<uintptr_t>(grad) % min(16, (int)sizeof(G) * kVec)) == 0;
+  float* mbase = p.moments ? reinterpret_cast<float*>(p.moments[st.t]) : nullptr;
+  if (st.vec) {
+    if (lane * kVec < st.D) {
+      Vec<W, kVec> v = ld_vec<W, kVec>(st.w + lane * kVec);
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) st.wv[e] = v.v[e];
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      const int j = lane + e * kWarp;
+      st.wv[e] = j < st.D ? st.w[j] : W(0);
+    }
+  }
+  if (p.optim == NEO_OPT_ROWWISE_ADAGRAD) {
+    st.m = mbase + st.row;
+    st.mr = *st.m;
+  } else if (p.optim == NEO_OPT_ADAGRAD) {
+    st.m = mbase + st.row * st.D;
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      const int j = st.vec ? lane * kVec + e : lane + e * kWarp;
+      st.mv[e] = j < st.D ? st.m[j] : 0.f;
+    }
+  }
+}
+
+template <typename G, int kVec>
+__device__ __forceinline__ void add_grad_row(const SegParams& p, const G* grad, int32_t bag, int32_t t,
+                                             int32_t D, int32_t doff, bool vec, int lane, float* acc) {
+  const int64_t b = (int64_t)bag - (int64_t)t * p.B;
+  const G* src = grad + b * p.grad_stride + doff;
+  if (vec) {
+    if (lane * kVec < D) {
+      Vec<G, kVec> v = ld_vec<G, kVec>(src + lane * kVec);
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(v.v[e]);
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) {
+      const int j = lane + e * kWarp;
+      if (j < D) acc[e] += Elem<G>::to_f(src[j]);
+    }
+  }
+}
+
+template <typename W, typename G, typename Key>
+__global__ void __launch_bounds__(kBwdWarps * kWarp)
+tbe_chunk_update_kernel(SegParams p) {
+  constexpr int kVec = 16 / sizeof(W);
+  constexpr int U = 4;
+  const unsigned full = 0xffffffffu;
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const Key* keys = reinterpret_cast<const Key*>(p.keys);
+  const int32_t* bags = p.bags;
+  const G* grad = reinterpret_cast<const G*>(p.grad);
+  const int64_t N = p.N;
+  const int64_t nchunks = (N + kWarp - 1) / kWarp;
+  const int64_t nwarps = (int64_t)gridDim.x * kBwdWarps;
+  const float lr = (float)p.lr, eps = (float)p.eps;
+  for (int64_t chunk = (int64_t)blockIdx.x * kBwdWarps + warp; chunk < nchunks; chunk += nwarps) {
+    const int64_t c0 = chunk * kWarp;
+    const int64_t j = c0 + lane;
+    const uint64_t key = j < N ? (uint64_t)keys[j] : ~0ull;
+    const int32_t bag = j < N ? bags[j] : 0;
+    uint64_t prev = __shfl_up_sync(full, key, 1);
+    if (lane == 0) prev = c0 > 0 ? (uint64_t)keys[c0 - 1] : ~key;
+    const unsigned bnd = __ballot_sync(full, key != prev);
+    if (bnd == 0) continue;  // chunk lies inside a segment started earlier
+    int h = __ffs(bnd) - 1;
+    SegState<W, float> cur;
+    load_seg_state<W, G, Key>(p, __shfl_sync(full, key, h), __shfl_sync(full, bag, h), lane, cur);
+    while (h < kWarp) {
+      const unsigned rest = h == kWarp - 1 ? 0u : (bnd & ~((2u << h) - 1u));
+      const int nh = rest ? __ffs(rest) - 1 : kWarp;
+      const uint64_t seg_key = __shfl_sync(full, key, h);
+      SegState<W, float> nxt;
+      nxt.live = false;
+      if (nh < kWarp)  // prefetch the next segment's row state
+        load_seg_state<W, G, Key>(p, __shfl_sync(full, key, nh), __shfl_sync(full, bag, nh), lane, nxt);
+      if (cur.live) {
+        float acc[kVec];
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
+        for (int e0 = h; e0 < nh; e0 += U) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int e = e0 + u;
+            const int32_t bg = __shfl_sync(full, bag, e < kWarp ? e : 0);
+            if (e < nh) add_grad_row<G, kVec>(p, grad, bg, cur.t, cur.D, cur.doff, cur.vec, lane, acc);
+          }
+        }
+        if (nh == kWarp) {  // the segment may continue into the following chunks
+          for (int64_t c = c0 + kWarp; c < N; c += kWarp) {
+            const int64_t jj = c + lane;
+            const bool same = jj < N && (uint64_t)keys[jj] == seg_key;
+            const int32_t b2 = same ? bags[jj] : 0;
+            const unsigned m = __ballot_sync(full, same);
+            const int cnt = m == full ? kWarp : __ffs(~m) - 1;
+            for (int e0 = 0; e0 < cnt; e0 += U) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) {
+                const int e = e0 + u;
+                const int32_t bg = __shfl_sync(full, b2, e < kWarp ? e : 0);
+                if (e < cnt) add_grad_row<G, kVec>(p, grad, bg, cur.t, cur.D, cur.doff, cur.vec, lane, acc);
+              }
+            }
+            if (cnt < kWarp) break;
+          }
+        }
+        // one optimizer step for the row (embedding.py:212-254)
+        bool nz = false;
+        float ss = 0.f;
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          nz |= acc[e] != 0.f;
+          ss += acc[e] * acc[e];
+        }
+        const bool any_nz = __any_sync(full, nz);
+        if (p.optim == NEO_OPT_SGD || any_nz) {
+          float denom = 1.f;
+          if (p.optim == NEO_OPT_ROWWISE_ADAGRAD) {
+            ss = warp_sum(ss);
+            const float m = cur.mr + ss / (float)cur.D;
+            if (lane == 0) *cur.m = m;
+            denom = sqrtf(m) + eps;
+          }
+          W out[kVec];
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            const float w = Elem<W>::to_f(cur.wv[e]);
+            float r;
+            if (p.optim == NEO_OPT_SGD) {
+              r = w - lr * acc[e];
+            } else if (p.optim == NEO_OPT_ROWWISE_ADAGRAD) {
+              r = w - lr * acc[e] / denom;
+            } else {
+              const float mj = cur.mv[e] + acc[e] * acc[e];
+              cur.mv[e] = mj;
+              r = w - lr * acc[e] / (sqrtf(mj) + eps);
+            }
+            out[e] = Elem<W>::from_f(r);
+          }
+          if (cur.vec) {
+            if (lane * kVec < cur.D) {
+              Vec<W, kVec> o;
+#pragma unroll
+              for (int e = 0; e < kVec; ++e) o.v[e] = out[e];
+              st_vec<W, kVec>(cur.w + lane * kVec, o);
+              if (p.optim == NEO_OPT_ADAGRAD) {
+#pragma unroll
+                for (int e = 0; e < kVec; ++e) cur.m[lane * kVec + e] = cur.mv[e];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < kVec; ++e) {
+              const int jx = lane + e * kWarp;
+              if (jx < cur.D) {
+                cur.w[jx] = out[e];
+                if (p.optim == NEO_OPT_ADAGRAD) cur.m[jx] = cur.mv[e];
+              }
+            }
+          }
+        }
+      }
+      cur = nxt;
+      h = nh;
+    }
+  }
+}
+
+template <typename W, typename G, typename Key>
+static int launch_chunks(const SegParams& p, cudaStream_t s) {
+  auto kern = tbe_chunk_update_kernel<W, G, Key>;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwdWarps * kWarp, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t chunks = (p.N + kWarp - 1) / kWarp;
+  const int64_t max_blocks = (chunks + kBwdWarps - 1) / kBwdWarps;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > max_blocks) grid = max_blocks;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, kBwdWarps * kWarp, 0, s>>>(p);
+  return check_launch("neo_tbe_backward(chunks)");
+}
+
 template <typename Key>
 __global__ void count_valid_kernel(const Key* keys, const int32_t* seg_starts,
                                    const int64_t* num_segs, int64_t total_rows, int64_t* out) {
@@ -332,13 +559,36 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
       cudaSuccess)
     return fail(NEO_E_CUDA, "neo_tbe_backward: radix sort failed");
   const Key* keys = kbuf.Current();
+  p.keys = keys;
+  p.bags = vbuf.Current();
+  const int wvec = weight_dtype == NEO_F16 ? 8 : 4;
+  const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
+                    p.max_dim <= kWarp * wvec && !out_count;
+  if (fast) {
+    const bool h = weight_dtype == NEO_F16;
+    switch (grad_dtype) {
+      case NEO_F32:
+        rc = h ? launch_chunks<__half, float, Key>(p, s) : launch_chunks<float, float, Key>(p, s);
+        break;
+      case NEO_BF16:
+        rc = h ? launch_chunks<__half, __nv_bfloat16, Key>(p, s)
+               : launch_chunks<float, __nv_bfloat16, Key>(p, s);
+        break;
+      case NEO_F16:
+        rc = h ? launch_chunks<__half, __half, Key>(p, s) : launch_chunks<float, __half, Key>(p, s);
+        break;
+      default:
+        return fail(NEO_E_ARG, "neo_tbe_backward: gradient dtype must be F32, BF16 or F16");
+    }
+    if (rc) return rc;
+    launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
+    return check_launch("neo_tbe_backward(finalize)");
+  }
   cub::CountingInputIterator<int32_t> it(0);
   temp_bytes = cub_temp_bytes<Key>(N);
   if (cub::DeviceSelect::If(temp, temp_bytes, it, starts, nseg, (int)N, HeadFlag<Key>{keys}, s) !=
       cudaSuccess)
     return fail(NEO_E_CUDA, "neo_tbe_backward: segment select failed");
-  p.keys = keys;
-  p.bags = vbuf.Current();
   p.seg_starts = starts;
   p.num_segs = nseg;
 

@@ -304,6 +304,18 @@ def gather_blocks(srcs: Sequence[torch.Tensor], counts: Sequence[int], dst: torc
     return dst
 
 
+def gather_blocks_dev(ptrs: torch.Tensor, counts: torch.Tensor, dst_offsets: torch.Tensor,
+                      dst: torch.Tensor) -> torch.Tensor:
+    """As gather_blocks, with the block table already on the device (int64
+    source pointers, counts, destination offsets) — no host sync."""
+    n = int(ptrs.numel())
+    if n:
+        capi.check(capi.lib().neo_gather_blocks(n, ptrs.data_ptr(), counts.data_ptr(), dst_offsets.data_ptr(),
+                                                dst.data_ptr(), dst.element_size(), _stream()),
+                   "neo_gather_blocks")
+    return dst
+
+
 def cast(x: torch.Tensor, dtype: torch.dtype, out: Optional[torch.Tensor] = None) -> torch.Tensor:
     """RNE element-wise conversion on device (neo_cast)."""
     out = torch.empty(x.shape, dtype=dtype, device=x.device) if out is None else out
