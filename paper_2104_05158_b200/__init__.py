@@ -25,8 +25,11 @@ from .embedding import (apply_adagrad, apply_optimizer, apply_rowwise_adagrad, a
                         backward_sort_aggregate, forward_pooled, fused_backward_update, fused_forward,
                         merge_row_gradients, quantize_fp16_roundtrip, storage_roundtrip,
                         train_step_reference)
-from .comms import (LaidOutBatch, ShardedState, ShardInput, WorkerSlice, bucketize_rowwise,  # noqa: F401
-                    from_twb, permute_TWB_to_WTB, permute_WTB_to_TWB, replicate_columnwise, to_wtb)
+from .comms import (LaidOutBatch, ShardedState, ShardInput, WorkerSlice, alltoall_redistribute,  # noqa: F401
+                    bucketize_rowwise, from_twb, permute_TWB_to_WTB, permute_WTB_to_TWB, reassemble_values,
+                    replicate_columnwise, to_wtb, train_step_sharded)
+from .plan import (Scheme, SchemeKind, Shard, ShardingPlan, TableAssignment, even_bounds,  # noqa: F401
+                   plan_from_json, plan_to_json, validate_plan)
 
 
 def load():

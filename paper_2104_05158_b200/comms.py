@@ -186,3 +186,138 @@ class ShardedState:
 
     shards: dict
     dp_replicas: dict
+
+
+# ---------------------------------------------------------------------------
+# redistribution and the sharded step on W logical ranks (comms.py:292-353,
+# comms.py:629-758), through the same engine the NCCL path runs
+
+
+def _local_batches(batch, W: int, index_dtype=torch.int64):
+    """Split a canonical global batch into the W workers' local batches
+    ((T, B) lengths, table-major ids on the device): the worker-major wire
+    order is one device block permute of the canonical (T, W, B) buffer."""
+    T, n = batch.num_tables, batch.num_samples
+    B = n // W
+    lengths = np.asarray(batch.lengths, dtype=np.int64)
+    ids = np.asarray(batch.indices, dtype=np.int64)
+    if ids.size:
+        L, I = tbe.permute_blocks(T, W, B, _dev(lengths.reshape(-1)), _dev(ids).to(index_dtype))
+    else:
+        L, I = _dev(lengths.reshape(-1)), torch.zeros(0, dtype=index_dtype, device=_device())
+    Lh = L.cpu().numpy().reshape(W, T, B)
+    per = Lh.reshape(W, -1).sum(axis=1)
+    starts = np.concatenate(([0], np.cumsum(per)))
+    return [(Lh[w], I[int(starts[w]):int(starts[w + 1])]) for w in range(W)]
+
+
+def _engine(model, plan, W, B, kind, init=None, dtype=torch.float64):
+    from .dist import LocalComm, ShardedEmbedding
+
+    return ShardedEmbedding(model, plan, LocalComm(W), B, dtype=dtype, optim=kind, init=init)
+
+
+def alltoall_redistribute(laidout, plan, model) -> list:
+    """Two-phase exchange (lengths, then ids) on W logical ranks; each worker
+    ends with its shards' global-batch inputs (comms.py:292-353)."""
+    from .plan import validate_plan
+
+    lay = laidout.layout
+    if _tag(lay.tag) != "WTB":
+        raise LayoutMismatch("redistribution consumes the WTB wire order")
+    if lay.workers != plan.num_workers or lay.tables != model.num_tables:
+        raise LayoutMismatch("batch layout does not match plan/model")
+    validate_plan(plan, model)
+    W, T, B = lay.workers, lay.tables, lay.local_batch
+    Lh = np.asarray(laidout.lengths, dtype=np.int64).reshape(W, T, B)
+    ids = _dev(np.asarray(laidout.indices, dtype=np.int64)) if len(laidout.indices) else \
+        torch.zeros(0, dtype=torch.int64, device=_device())
+    per = Lh.reshape(W, -1).sum(axis=1)
+    starts = np.concatenate(([0], np.cumsum(per)))
+    batches = [(Lh[w], ids[int(starts[w]):int(starts[w + 1])]) for w in range(W)]
+    eng = _engine(model, plan, W, B, "sgd")
+    per_rank = eng.redistribute(batches)
+    by_id = {a.table_id: a for a in plan.assignments}
+    slices = [WorkerSlice(worker=v) for v in range(W)]
+    for t, table in enumerate(model.tables):
+        a = by_id[table.id]
+        kind = getattr(a.scheme.kind, "value", a.scheme.kind)
+        if kind == "data_parallel":
+            for v in range(W):
+                L, I = per_rank[v]["dp"][t]
+                slices[v].inputs.append(ShardInput(table.id, a.shards[0], L, I, sample_base=v * B))
+            continue
+        shards = list(a.shards)
+        if kind == "row_wise":
+            shards = sorted(shards, key=lambda s: tuple(s.rows))
+        for s in shards:
+            L, I = per_rank[s.worker]["shards"][(t, list(a.shards).index(s))]
+            slices[s.worker].inputs.append(ShardInput(table.id, s, L, I))
+    return slices
+
+
+def _spec_prec(spec) -> str:
+    return getattr(spec.value_precision, "value", spec.value_precision)
+
+
+def train_step_sharded(model, plan, batch, cfg, seed: int = 0, zero_init: bool = False):
+    """One iteration across W logical workers through the sharded engine
+    (comms.py:629-737): input exchange, fused forward per worker, pooled
+    exchange + assembly, backward exchange, fused update per shard, DP
+    gradient all-reduce + identical update.  Returns (outputs, ShardedState)."""
+    from .embedding import build_tables
+    from .plan import validate_plan
+    from .spec import EmbeddingTable, kind_value
+
+    validate_plan(plan, model)
+    batch.validate_against(model)
+    W = plan.num_workers
+    if batch.num_samples % W:
+        raise LayoutMismatch("global batch must split evenly across workers")
+    n = batch.num_samples
+    B = n // W
+    kind = kind_value(cfg.kind)
+    full = build_tables(model, cfg, seed, zero_init=zero_init)
+
+    def init(t, rows, cols):
+        return torch.from_numpy(np.ascontiguousarray(full[t].values[rows[0]:rows[1], cols[0]:cols[1]]))
+
+    eng = _engine(model, plan, W, B, kind, init=init)
+    pooled = eng.step(_local_batches(batch, W), lr=cfg.lr, eps=cfg.eps)
+    out = torch.cat(pooled, dim=0).cpu().numpy() if model.num_tables else np.zeros((n, 0))
+    state = ShardedState(shards={}, dp_replicas={})
+    lay = eng.lay
+    for slot, st in enumerate(eng.states):
+        for s, w, m in eng.shard_tensors(slot):
+            spec = model.tables[s.table]
+            if _spec_prec(spec) == "FP16":
+                tbe.fp16_roundtrip_(w)
+            state.shards[(s.table_id, s.index)] = EmbeddingTable(
+                spec, w.cpu().numpy(), None if m is None else m.cpu().numpy(), row_base=s.rows[0],
+                col_base=s.cols[0])
+        if st.dp_group is not None:
+            for t, w, m in zip(lay.dp_tables, st.dp_group.weights, st.dp_group.moments):
+                spec = model.tables[t]
+                if _spec_prec(spec) == "FP16":
+                    tbe.fp16_roundtrip_(w)
+                state.dp_replicas.setdefault(spec.id, []).append(
+                    EmbeddingTable(spec, w.cpu().numpy(), None if m is None else m.cpu().numpy()))
+    return out, state
+
+
+def reassemble_values(model, plan, state) -> list:
+    """Stitch shard values into full (H, D) matrices; DP from replica 0
+    (comms.py:740-758)."""
+    out = []
+    for table in model.tables:
+        a = plan.assignment_for(table.id)
+        if getattr(a.scheme.kind, "value", a.scheme.kind) == "data_parallel":
+            out.append(state.dp_replicas[table.id][0].values.copy())
+            continue
+        full = np.zeros((table.num_rows, table.dim), dtype=np.float64)
+        for i, s in enumerate(a.shards):
+            r0, r1 = s.rows if s.rows else (0, table.num_rows)
+            c0, c1 = s.cols if s.cols else (0, table.dim)
+            full[r0:r1, c0:c1] = state.shards[(table.id, i)].values
+        out.append(full)
+    return out

@@ -232,230 +232,293 @@ tbe_segment_kernel(SegParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// 4'. fast path: chunked segment walk (f32/f16 tables, rows of <= 32 vectors,
-// SUM pooling, UPDATE mode).  Each warp owns a chunk of 32 consecutive sorted
-// (key, bag) entries and processes every segment that STARTS in it (walking
-// past the chunk end for the last one), so segment boundaries come from one
-// coalesced key load + a shuffle instead of a compaction pass, and the weight
-// row / moment of the next segment is prefetched while the current segment's
-// upstream rows are gathered.  Accumulation stays in sorted (= buffer) order.
+// 4'. fast path: streamed segment walk (f32/f16 tables, rows of <= 32 16-byte
+// vectors, SUM pooling, UPDATE mode).
+//
+// Each warp owns a chunk of 32 consecutive sorted (key, bag) entries and
+// every segment that STARTS in it (walking past the chunk end for the last
+// one); segment boundaries come from one coalesced key load + a shuffle.  The
+// warp runs two cursors over that entry stream: a producer LEAD entries ahead
+// issues cp.async copies of each entry's upstream row (and, at a segment
+// head, of the segment's weight row and moment) into per-warp shared-memory
+// rings, one commit group per entry; the consumer waits for the group of its
+// entry, accumulates the row, and at the next head applies the optimizer to
+// the staged weight row and stores it.  Every lane only ever reads the bytes
+// it copied itself, so no warp barrier guards the rings, and LEAD rows per
+// warp stay in flight without occupying registers.  Accumulation order is the
+// sorted (= buffer) order.
 
-template <typename W, typename Acc>
-struct SegState {
-  int64_t row;
-  W* w;       // row pointer
-  Acc* m;     // row-wise: &moment[row]; element-wise: moment row
-  int32_t t, D, doff;
-  bool vec, live;
-  W wv[16 / sizeof(W)];
-  Acc mv[16 / sizeof(W)];
-  Acc mr;
+constexpr int kLead = 7;               // entries in flight per warp
+constexpr int kGRing = kLead + 1;      // upstream-row slots
+constexpr int kWRing = kLead + 3;      // open-segment slots (>= kLead + 2)
+constexpr int kStreamWarps = 4;        // warps per CTA
+
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+struct SegMeta {   // written by lane 0 of the producer, read by the consumer
+  uint64_t w;      // weight row pointer
+  uint64_t m;      // moment pointer (row-wise scalar or element-wise row)
+  int32_t D;
+  int32_t vec;     // 1: lane owns columns [lane*VEC, +VEC); 0: lane + e*32
+};
+
+template <typename W, typename G>
+struct StreamSmem {
+  static constexpr int kVec = 16 / sizeof(W);
+  static constexpr int kGBytes = kVec * sizeof(G);  // upstream bytes per lane per row
+  unsigned char g[kGRing][kWarp][kGBytes];
+  unsigned char w[kWRing][kWarp][16];
+  float mr[kWRing];               // row-wise moment
+  SegMeta seg[kWRing];
+  int32_t ent[kGRing];            // (head << 16) | seg slot
 };
 
 template <typename W, typename G, typename Key>
-__device__ __forceinline__ void load_seg_state(const SegParams& p, uint64_t key, int32_t bag, int lane,
-                                               SegState<W, float>& st) {
-  constexpr int kVec = 16 / sizeof(W);
-  st.live = key < (uint64_t)p.total_rows;
-  if (!st.live) return;
-  st.t = bag / (int32_t)p.B;
-  st.row = (int64_t)key - p.row_offsets[st.t];
-  st.doff = p.dim_offsets[st.t];
-  st.D = p.dim_offsets[st.t + 1] - st.doff;
-  W* wbase = reinterpret_cast<W*>(p.weights[st.t]);
-  st.w = wbase + st.row * st.D;
-  const G* grad = reinterpret_cast<const G*>(p.grad);
-  st.vec = (st.D % kVec) == 0 && aligned16(wbase) && (st.doff % kVec) == 0 &&
-           (p.grad_stride % kVec) == 0 &&
-           (reinterpret_cast<uintptr_t>(grad) % min(16, (int)sizeof(G) * kVec)) == 0;
-  float* mbase = p.moments ? reinterpret_cast<float*>(p.moments[st.t]) : nullptr;
-  if (st.vec) {
-    if (lane * kVec < st.D) {
-      Vec<W, kVec> v = ld_vec<W, kVec>(st.w + lane * kVec);
-#pragma unroll
-      for (int e = 0; e < kVec; ++e) st.wv[e] = v.v[e];
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < kVec; ++e) {
-      const int j = lane + e * kWarp;
-      st.wv[e] = j < st.D ? st.w[j] : W(0);
-    }
-  }
-  if (p.optim == NEO_OPT_ROWWISE_ADAGRAD) {
-    st.m = mbase + st.row;
-    st.mr = *st.m;
-  } else if (p.optim == NEO_OPT_ADAGRAD) {
-    st.m = mbase + st.row * st.D;
-#pragma unroll
-    for (int e = 0; e < kVec; ++e) {
-      const int j = st.vec ? lane * kVec + e : lane + e * kWarp;
-      st.mv[e] = j < st.D ? st.m[j] : 0.f;
-    }
-  }
-}
-
-template <typename G, int kVec>
-__device__ __forceinline__ void add_grad_row(const SegParams& p, const G* grad, int32_t bag, int32_t t,
-                                             int32_t D, int32_t doff, bool vec, int lane, float* acc) {
-  const int64_t b = (int64_t)bag - (int64_t)t * p.B;
-  const G* src = grad + b * p.grad_stride + doff;
-  if (vec) {
-    if (lane * kVec < D) {
-      Vec<G, kVec> v = ld_vec<G, kVec>(src + lane * kVec);
-#pragma unroll
-      for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(v.v[e]);
-    }
-  } else {
-#pragma unroll
-    for (int e = 0; e < kVec; ++e) {
-      const int j = lane + e * kWarp;
-      if (j < D) acc[e] += Elem<G>::to_f(src[j]);
-    }
-  }
-}
-
-template <typename W, typename G, typename Key>
-__global__ void __launch_bounds__(kBwdWarps * kWarp)
-tbe_chunk_update_kernel(SegParams p) {
-  constexpr int kVec = 16 / sizeof(W);
-  constexpr int U = 4;
+__global__ void __launch_bounds__(kStreamWarps * kWarp)
+tbe_stream_update_kernel(SegParams p) {
+  using SM = StreamSmem<W, G>;
+  constexpr int kVec = SM::kVec;
+  constexpr int kGB = SM::kGBytes;
   const unsigned full = 0xffffffffu;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  SM& sm = reinterpret_cast<SM*>(smem_raw)[warp];
   const Key* keys = reinterpret_cast<const Key*>(p.keys);
   const int32_t* bags = p.bags;
   const G* grad = reinterpret_cast<const G*>(p.grad);
   const int64_t N = p.N;
+  const uint64_t total = (uint64_t)p.total_rows;
   const int64_t nchunks = (N + kWarp - 1) / kWarp;
-  const int64_t nwarps = (int64_t)gridDim.x * kBwdWarps;
+  const int64_t nwarps = (int64_t)gridDim.x * kStreamWarps;
   const float lr = (float)p.lr, eps = (float)p.eps;
-  for (int64_t chunk = (int64_t)blockIdx.x * kBwdWarps + warp; chunk < nchunks; chunk += nwarps) {
+  const int optim = p.optim;
+  const bool gvec_ok = (p.grad_stride % kVec) == 0 &&
+                       (reinterpret_cast<uintptr_t>(grad) % (kGB < 16 ? kGB : 16)) == 0;
+
+  for (int64_t chunk = (int64_t)blockIdx.x * kStreamWarps + warp; chunk < nchunks; chunk += nwarps) {
     const int64_t c0 = chunk * kWarp;
-    const int64_t j = c0 + lane;
-    const uint64_t key = j < N ? (uint64_t)keys[j] : ~0ull;
-    const int32_t bag = j < N ? bags[j] : 0;
-    uint64_t prev = __shfl_up_sync(full, key, 1);
-    if (lane == 0) prev = c0 > 0 ? (uint64_t)keys[c0 - 1] : ~key;
-    const unsigned bnd = __ballot_sync(full, key != prev);
-    if (bnd == 0) continue;  // chunk lies inside a segment started earlier
-    int h = __ffs(bnd) - 1;
-    SegState<W, float> cur;
-    load_seg_state<W, G, Key>(p, __shfl_sync(full, key, h), __shfl_sync(full, bag, h), lane, cur);
-    while (h < kWarp) {
-      const unsigned rest = h == kWarp - 1 ? 0u : (bnd & ~((2u << h) - 1u));
-      const int nh = rest ? __ffs(rest) - 1 : kWarp;
-      const uint64_t seg_key = __shfl_sync(full, key, h);
-      SegState<W, float> nxt;
-      nxt.live = false;
-      if (nh < kWarp)  // prefetch the next segment's row state
-        load_seg_state<W, G, Key>(p, __shfl_sync(full, key, nh), __shfl_sync(full, bag, nh), lane, nxt);
-      if (cur.live) {
-        float acc[kVec];
-#pragma unroll
-        for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
-        for (int e0 = h; e0 < nh; e0 += U) {
-#pragma unroll
-          for (int u = 0; u < U; ++u) {
-            const int e = e0 + u;
-            const int32_t bg = __shfl_sync(full, bag, e < kWarp ? e : 0);
-            if (e < nh) add_grad_row<G, kVec>(p, grad, bg, cur.t, cur.D, cur.doff, cur.vec, lane, acc);
-          }
+    // window of 32 entries for the producer
+    int64_t wbase = c0;
+    uint64_t wkey = c0 + lane < N ? (uint64_t)keys[c0 + lane] : ~0ull;
+    int32_t wbag = c0 + lane < N ? bags[c0 + lane] : 0;
+    uint64_t prev = __shfl_up_sync(full, wkey, 1);
+    if (lane == 0) prev = c0 > 0 ? (uint64_t)keys[c0 - 1] : ~wkey;
+    unsigned wbnd = __ballot_sync(full, wkey != prev);
+    if (wbnd == 0) continue;
+    const int64_t e_begin = c0 + (__ffs(wbnd) - 1);
+    if (__shfl_sync(full, wkey, __ffs(wbnd) - 1) >= total) continue;  // only invalid ids here
+
+    // producer state
+    int64_t pe = e_begin;
+    bool done = false;
+    int64_t e_end = -1;
+    int wslot = -1;
+    int32_t pt = 0, pdoff = 0, pD = 0;
+    bool pgvec = false;
+
+    auto produce = [&]() {
+      if (!done) {
+        if (pe - wbase >= kWarp) {  // slide the window
+          const uint64_t last = __shfl_sync(full, wkey, kWarp - 1);
+          wbase += kWarp;
+          wkey = wbase + lane < N ? (uint64_t)keys[wbase + lane] : ~0ull;
+          wbag = wbase + lane < N ? bags[wbase + lane] : 0;
+          uint64_t pv = __shfl_up_sync(full, wkey, 1);
+          if (lane == 0) pv = last;
+          wbnd = __ballot_sync(full, wkey != pv);
         }
-        if (nh == kWarp) {  // the segment may continue into the following chunks
-          for (int64_t c = c0 + kWarp; c < N; c += kWarp) {
-            const int64_t jj = c + lane;
-            const bool same = jj < N && (uint64_t)keys[jj] == seg_key;
-            const int32_t b2 = same ? bags[jj] : 0;
-            const unsigned m = __ballot_sync(full, same);
-            const int cnt = m == full ? kWarp : __ffs(~m) - 1;
-            for (int e0 = 0; e0 < cnt; e0 += U) {
+        const int l = (int)(pe - wbase);
+        const bool head = (wbnd >> l) & 1u;
+        const uint64_t k = __shfl_sync(full, wkey, l);
+        const int32_t bag = __shfl_sync(full, wbag, l);
+        if (pe >= N || k >= total || (head && pe >= c0 + kWarp)) {
+          done = true;
+          e_end = pe;
+        } else {
+          if (head) {  // new segment: stage its weight row + moment
+            wslot = wslot + 1 == kWRing ? 0 : wslot + 1;
+            pt = bag / (int32_t)p.B;
+            const int64_t row = (int64_t)k - p.row_offsets[pt];
+            pdoff = p.dim_offsets[pt];
+            pD = p.dim_offsets[pt + 1] - pdoff;
+            W* wrow = reinterpret_cast<W*>(p.weights[pt]) + row * pD;
+            float* mbase = p.moments ? reinterpret_cast<float*>(p.moments[pt]) : nullptr;
+            float* mptr = optim == NEO_OPT_ROWWISE_ADAGRAD ? mbase + row
+                          : optim == NEO_OPT_ADAGRAD      ? mbase + row * pD
+                                                          : nullptr;
+            const bool wvec = (pD % kVec) == 0 && aligned16(reinterpret_cast<const void*>(p.weights[pt]));
+            pgvec = wvec && gvec_ok && (pdoff % kVec) == 0;
+            const bool vec = wvec && pgvec;
+            if (vec) {
+              if (lane * kVec < pD) cp_async(&sm.w[wslot][lane][0], wrow + lane * kVec, 16);
+            } else {  // unaligned table: synchronous strided staging
+              W* ws = reinterpret_cast<W*>(&sm.w[wslot][lane][0]);
 #pragma unroll
-              for (int u = 0; u < U; ++u) {
-                const int e = e0 + u;
-                const int32_t bg = __shfl_sync(full, b2, e < kWarp ? e : 0);
-                if (e < cnt) add_grad_row<G, kVec>(p, grad, bg, cur.t, cur.D, cur.doff, cur.vec, lane, acc);
+              for (int e = 0; e < kVec; ++e) {
+                const int j = lane + e * kWarp;
+                ws[e] = j < pD ? wrow[j] : W(0);
               }
             }
-            if (cnt < kWarp) break;
-          }
-        }
-        // one optimizer step for the row (embedding.py:212-254)
-        bool nz = false;
-        float ss = 0.f;
-#pragma unroll
-        for (int e = 0; e < kVec; ++e) {
-          nz |= acc[e] != 0.f;
-          ss += acc[e] * acc[e];
-        }
-        const bool any_nz = __any_sync(full, nz);
-        if (p.optim == NEO_OPT_SGD || any_nz) {
-          float denom = 1.f;
-          if (p.optim == NEO_OPT_ROWWISE_ADAGRAD) {
-            ss = warp_sum(ss);
-            const float m = cur.mr + ss / (float)cur.D;
-            if (lane == 0) *cur.m = m;
-            denom = sqrtf(m) + eps;
-          }
-          W out[kVec];
-#pragma unroll
-          for (int e = 0; e < kVec; ++e) {
-            const float w = Elem<W>::to_f(cur.wv[e]);
-            float r;
-            if (p.optim == NEO_OPT_SGD) {
-              r = w - lr * acc[e];
-            } else if (p.optim == NEO_OPT_ROWWISE_ADAGRAD) {
-              r = w - lr * acc[e] / denom;
-            } else {
-              const float mj = cur.mv[e] + acc[e] * acc[e];
-              cur.mv[e] = mj;
-              r = w - lr * acc[e] / (sqrtf(mj) + eps);
+            if (lane == 0) {
+              if (optim == NEO_OPT_ROWWISE_ADAGRAD) cp_async(&sm.mr[wslot], mptr, 4);
+              sm.seg[wslot] = SegMeta{reinterpret_cast<uint64_t>(wrow), reinterpret_cast<uint64_t>(mptr), pD,
+                                      vec ? 1 : 0};
             }
-            out[e] = Elem<W>::from_f(r);
+            pgvec = vec;
           }
-          if (cur.vec) {
-            if (lane * kVec < cur.D) {
-              Vec<W, kVec> o;
-#pragma unroll
-              for (int e = 0; e < kVec; ++e) o.v[e] = out[e];
-              st_vec<W, kVec>(cur.w + lane * kVec, o);
-              if (p.optim == NEO_OPT_ADAGRAD) {
-#pragma unroll
-                for (int e = 0; e < kVec; ++e) cur.m[lane * kVec + e] = cur.mv[e];
+          const int gs = (int)(pe % kGRing);
+          const G* grow = grad + ((int64_t)bag - (int64_t)pt * p.B) * p.grad_stride + pdoff;
+          if (pgvec) {
+            if (lane * kVec < pD) {
+              if constexpr (kGB == 32) {
+                cp_async(&sm.g[gs][lane][0], grow + lane * kVec, 16);
+                cp_async(&sm.g[gs][lane][16], grow + lane * kVec + kVec / 2, 16);
+              } else {
+                cp_async(&sm.g[gs][lane][0], grow + lane * kVec, kGB);
               }
             }
           } else {
+            G* gsm = reinterpret_cast<G*>(&sm.g[gs][lane][0]);
 #pragma unroll
             for (int e = 0; e < kVec; ++e) {
-              const int jx = lane + e * kWarp;
-              if (jx < cur.D) {
-                cur.w[jx] = out[e];
-                if (p.optim == NEO_OPT_ADAGRAD) cur.m[jx] = cur.mv[e];
-              }
+              const int j = lane + e * kWarp;
+              gsm[e] = j < pD ? grow[j] : G(0);
+            }
+          }
+          if (lane == 0) sm.ent[gs] = ((head ? 1 : 0) << 16) | wslot;
+          ++pe;
+        }
+      }
+      cp_commit();
+    };
+
+    float acc[kVec];
+#pragma unroll
+    for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
+    int cur = -1;
+
+    auto finalize = [&](int slot) {
+      const SegMeta sg = sm.seg[slot];
+      bool nz = false;
+      float ss = 0.f;
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) {
+        nz |= acc[e] != 0.f;
+        ss += acc[e] * acc[e];
+      }
+      const bool any_nz = __any_sync(full, nz);
+      if (optim == NEO_OPT_SGD || any_nz) {
+        float denom = 1.f;
+        if (optim == NEO_OPT_ROWWISE_ADAGRAD) {
+          ss = warp_sum(ss);
+          const float m = __shfl_sync(full, sm.mr[slot], 0) + ss / (float)sg.D;
+          if (lane == 0) *reinterpret_cast<float*>(sg.m) = m;
+          denom = sqrtf(m) + eps;
+        }
+        const W* wsm = reinterpret_cast<const W*>(&sm.w[slot][lane][0]);
+        W out[kVec];
+        float mo[kVec];
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          const float w = Elem<W>::to_f(wsm[e]);
+          float r;
+          if (optim == NEO_OPT_SGD) {
+            r = w - lr * acc[e];
+          } else if (optim == NEO_OPT_ROWWISE_ADAGRAD) {
+            r = w - lr * acc[e] / denom;
+          } else {  // element-wise state read here (not staged: off the benchmark path)
+            const int j = sg.vec ? lane * kVec + e : lane + e * kWarp;
+            const float mj = (j < sg.D ? reinterpret_cast<const float*>(sg.m)[j] : 0.f) + acc[e] * acc[e];
+            mo[e] = mj;
+            r = w - lr * acc[e] / (sqrtf(mj) + eps);
+          }
+          out[e] = Elem<W>::from_f(r);
+        }
+        W* wrow = reinterpret_cast<W*>(sg.w);
+        float* mrow = reinterpret_cast<float*>(sg.m);
+        if (sg.vec) {
+          if (lane * kVec < sg.D) {
+            Vec<W, kVec> o;
+#pragma unroll
+            for (int e = 0; e < kVec; ++e) o.v[e] = out[e];
+            st_vec<W, kVec>(wrow + lane * kVec, o);
+            if (optim == NEO_OPT_ADAGRAD) {
+#pragma unroll
+              for (int e = 0; e < kVec; ++e) mrow[lane * kVec + e] = mo[e];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            const int j = lane + e * kWarp;
+            if (j < sg.D) {
+              wrow[j] = out[e];
+              if (optim == NEO_OPT_ADAGRAD) mrow[j] = mo[e];
             }
           }
         }
       }
-      cur = nxt;
-      h = nh;
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
+    };
+
+    for (int i = 0; i < kLead; ++i) produce();  // fill the pipeline
+    for (int64_t ce = e_begin;; ++ce) {
+      produce();
+      if (done && ce >= e_end) break;
+      cp_wait<kLead>();
+      __syncwarp();
+      const int gs = (int)(ce % kGRing);
+      const int ent = sm.ent[gs];
+      if (ent >> 16) {
+        if (cur >= 0) finalize(cur);
+        cur = ent & 0xffff;
+      }
+      const SegMeta& sg = sm.seg[cur];
+      const G* gsm = reinterpret_cast<const G*>(&sm.g[gs][lane][0]);
+      const bool live = sg.vec ? lane * kVec < sg.D : true;
+      if (live) {
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
+      }
+      __syncwarp();
     }
+    if (cur >= 0) finalize(cur);
+    cp_wait<0>();
+    __syncwarp();
   }
 }
 
 template <typename W, typename G, typename Key>
-static int launch_chunks(const SegParams& p, cudaStream_t s) {
-  auto kern = tbe_chunk_update_kernel<W, G, Key>;
+static int launch_stream(const SegParams& p, cudaStream_t s) {
+  auto kern = tbe_stream_update_kernel<W, G, Key>;
+  const size_t smem = sizeof(StreamSmem<W, G>) * kStreamWarps;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve shared memory");
   int dev = 0, sms = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBwdWarps * kWarp, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamWarps * kWarp, smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t chunks = (p.N + kWarp - 1) / kWarp;
-  const int64_t max_blocks = (chunks + kBwdWarps - 1) / kBwdWarps;
+  const int64_t max_blocks = (chunks + kStreamWarps - 1) / kStreamWarps;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > max_blocks) grid = max_blocks;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, kBwdWarps * kWarp, 0, s>>>(p);
-  return check_launch("neo_tbe_backward(chunks)");
+  kern<<<(unsigned)grid, kStreamWarps * kWarp, smem, s>>>(p);
+  return check_launch("neo_tbe_backward(stream)");
 }
 
 template <typename Key>
@@ -568,14 +631,14 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
     const bool h = weight_dtype == NEO_F16;
     switch (grad_dtype) {
       case NEO_F32:
-        rc = h ? launch_chunks<__half, float, Key>(p, s) : launch_chunks<float, float, Key>(p, s);
+        rc = h ? launch_stream<__half, float, Key>(p, s) : launch_stream<float, float, Key>(p, s);
         break;
       case NEO_BF16:
-        rc = h ? launch_chunks<__half, __nv_bfloat16, Key>(p, s)
-               : launch_chunks<float, __nv_bfloat16, Key>(p, s);
+        rc = h ? launch_stream<__half, __nv_bfloat16, Key>(p, s)
+               : launch_stream<float, __nv_bfloat16, Key>(p, s);
         break;
       case NEO_F16:
-        rc = h ? launch_chunks<__half, __half, Key>(p, s) : launch_chunks<float, __half, Key>(p, s);
+        rc = h ? launch_stream<__half, __half, Key>(p, s) : launch_stream<float, __half, Key>(p, s);
         break;
       default:
         return fail(NEO_E_ARG, "neo_tbe_backward: gradient dtype must be F32, BF16 or F16");

@@ -194,19 +194,22 @@ def test_group_forward_f32_tolerance(pkg, wdtype, idtype):
         col += D
 
 
+# dims sets: the first has a 256-wide f32 table (general segment kernel), the
+# second fits the streamed fast path (incl. an unaligned D=100 table)
+@pytest.mark.parametrize("dims,rows", [([64, 128, 32, 256], [3000, 5000, 800, 2000]),
+                                       ([64, 128, 32, 8, 100], [3000, 5000, 40, 2000, 700])])
 @pytest.mark.parametrize("kind", ["rowwise_adagrad", "adagrad", "sgd"])
 @pytest.mark.parametrize("gdtype", [torch.float32, torch.bfloat16])
-def test_group_backward_update_f32_tolerance(pkg, kind, gdtype):
+@pytest.mark.parametrize("wdtype", [torch.float32, torch.float16])
+def test_group_backward_update_f32_tolerance(pkg, kind, gdtype, wdtype, dims, rows):
     from paper_2104_05158_b200 import tbe
 
     rng = np.random.default_rng(11)
-    dims = [64, 128, 32, 256]
-    rows = [3000, 5000, 800, 2000]
     B = 1024
     lengths, idx = _random_group_case(rng, len(dims), rows, dims, B, 24)
-    grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim=kind)
+    grp = tbe.TableGroup(rows, dims, dtype=wdtype, optim=kind)
     for w in grp.weights:
-        w.copy_(torch.randn(w.shape, device="cuda"))
+        w.copy_(torch.randn(w.shape, device="cuda").to(wdtype))
     w0 = [w.double().cpu().numpy() for w in grp.weights]
     grad = torch.randn((B, grp.total_dim), device="cuda").to(gdtype)
     off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
@@ -221,7 +224,8 @@ def test_group_backward_update_f32_tolerance(pkg, kind, gdtype):
         ids, g = O.backward_aggregate_c(lengths[t], idx[tab_off[t]:tab_off[t + 1]], np.ascontiguousarray(up[:, col:col + D]))
         O.apply_c(kind, v, m, ids, g, lr, eps)
         got = grp.weights[t].double().cpu().numpy()
-        tol = 1e-5 * (np.abs(v) + np.abs(v - w0[t])) + 1e-7
+        ulp = 2.0 ** -11 * np.abs(v) if wdtype == torch.float16 else 0.0  # one storage rounding
+        tol = 1e-5 * (np.abs(v) + np.abs(v - w0[t])) + 1e-7 + ulp
         assert (np.abs(got - v) <= tol).all(), (kind, t, np.abs(got - v).max())
         if m is not None:
             # moment error scales with (sum of |upstream| terms)^2, not with m
