@@ -274,7 +274,7 @@ struct SegMeta {   // written by lane 0 of the producer, read by the consumer
 };
 
 template <typename W, typename G>
-struct StreamSmem {
+struct alignas(16) StreamSmem {
   static constexpr int kVec = 16 / sizeof(W);
   static constexpr int kGBytes = kVec * sizeof(G);  // upstream bytes per lane per row
   unsigned char g[kGRing][kWarp][kGBytes];
