@@ -124,8 +124,9 @@ class RankState:
     dp_group: Optional[tbe.TableGroup] = None    # replicated DP tables
     dp_dense: Optional[torch.Tensor] = None      # flat dense DP gradient buffer
     dp_dense_views: list = field(default_factory=list)
-    # per-step scratch
-    scratch: dict = field(default_factory=dict)
+    bufs: dict = field(default_factory=dict)     # persistent device buffers (grow-only)
+    cache: dict = field(default_factory=dict)    # packed piece tables keyed by buffer pointers
+    sc: dict = field(default_factory=dict)       # per-step values
 
 
 def _dtype_bytes(dt) -> int:
@@ -139,8 +140,9 @@ class ShardedEmbedding:
     (reference or ours); comm: NcclComm / LocalComm; local_batch: B per rank.
     dtype: table storage (f32 / f16 production, f64 oracle-order).
     fwd_comm / bwd_comm: wire dtype of the pooled all-to-all (None = the
-    compute dtype; torch.float16 / torch.bfloat16 for quantized comm,
-    PAPER.md:656).
+    accumulator dtype; torch.float16 / torch.bfloat16 for the paper's
+    quantized communication).  Pooled outputs returned by
+    ``step`` live in persistent buffers valid until the next step.
     """
 
     def __init__(self, model, plan, comm: Comm, local_batch: int, device=None, dtype=torch.float32,
@@ -163,6 +165,20 @@ class ShardedEmbedding:
         self.bwd_comm = bwd_comm or self.acc
         self.index_dtype = index_dtype
         self.T = len(model.tables)
+        lay = self.lay
+        self.widths = [lay.width(w) for w in range(self.W)]
+        # send order of input blocks: destination-major, then the destination's shards
+        self.send_blocks = [(v, s) for v in range(self.W) for s in lay.owned[v]]
+        self.rw_slot = {}
+        for t, bounds in lay.rw_bounds.items():
+            for s in (s for v in range(self.W) for s in lay.owned[v] if s.table == t):
+                self.rw_slot[(t, s.index)] = bounds.index(s.rows)
+        self.dp_cols = {}
+        c = 0
+        for t in lay.dp_tables:
+            self.dp_cols[t] = c
+            c += lay.dims[t]
+        self.dp_width = c
         self.states = [self._make_state(r, init) for r in comm.ranks]
 
     # -- construction ----------------------------------------------------
@@ -193,104 +209,107 @@ class ShardedEmbedding:
                 off += sz
         return st
 
+    def _buf(self, st: RankState, name: str, numel: int, dtype) -> torch.Tensor:
+        b = st.bufs.get(name)
+        if b is None or b.numel() < max(numel, 1) or b.dtype != dtype:
+            b = torch.empty(max(int(numel), 1), dtype=dtype, device=self.device)
+            st.bufs[name] = b
+        return b
+
     # -- byte contract ---------------------------------------------------
     def pooled_send_bytes(self, rank: int, elem_bytes: Optional[int] = None) -> int:
         """Per-rank pooled all-to-all send bytes excluding self: sum over
         local shards of width x (n - B) x elem (comms.py:366-392 for TW/CW;
         row-wise partial pools ride the same exchange, (k-1)/k n D for k=W)."""
         e = elem_bytes or _dtype_bytes(self.fwd_comm)
-        return self.lay.width(rank) * (self.n - self.B) * e
+        return self.widths[rank] * (self.n - self.B) * e
 
     # -- the step --------------------------------------------------------
-    def step(self, batches: Sequence, lr: float, eps: float = 0.0,
-             upstream_fn: Optional[Callable] = None, timers: Optional[dict] = None):
-        """One training step.  batches[i] = (lengths (T, B) int64 numpy,
-        ids device tensor, table-major) for local rank slot i.  Returns the
-        pooled (B, sum D) outputs per local rank (model table order).
-        upstream_fn(pooled) -> gradient (default: ones, the reference's
-        sum-of-outputs loss)."""
-        lay, W, B = self.lay, self.W, self.B
+    def _exchange_inputs(self, batches: Sequence) -> None:
+        W, B = self.W, self.B
         S = self.states
-        # ---- phase 1: local bucketise + pack lengths
-        for st, (lengths, ids) in zip(S, batches):
-            self._pack_lengths(st, np.asarray(lengths, dtype=np.int64), ids)
-        self.comm.all_to_all([st.scratch["recv_len"] for st in S], [st.scratch["send_len"] for st in S],
-                             [st.scratch["len_out_splits"] for st in S], [st.scratch["len_in_splits"] for st in S])
-        # ---- phase 2: counts (one host sync for all local ranks)
+        for st, bt in zip(S, batches):
+            self._pack_lengths(st, bt)
+        self.comm.all_to_all([st.sc["recv_len"] for st in S], [st.sc["send_len"] for st in S],
+                             [[len(self.lay.owned[st.rank]) * B] * W for st in S],
+                             [[len(self.lay.owned[v]) * B for v in range(W)] for st in S])
         cnts = []
         for st in S:
-            nS = len(lay.owned[st.rank])
-            rl = st.scratch["recv_len"].view(W, nS * B) if nS else None
-            recv = rl.sum(dim=1) if nS else torch.zeros(W, dtype=torch.int64, device=self.device)
-            cnts.append(torch.cat([st.scratch["send_counts"], recv]))
-        host = torch.stack(cnts).cpu().numpy()
+            nS = len(self.lay.owned[st.rank])
+            recv = st.sc["recv_len"][:W * nS * B].view(W, nS * B).sum(dim=1) if nS else \
+                torch.zeros(W, dtype=torch.int64, device=self.device)
+            cnts.append(torch.cat([st.sc["send_counts"], recv]))
+        host = torch.stack(cnts).cpu().numpy()  # the one host sync of the step
         for st, h in zip(S, host):
-            st.scratch["idx_in_splits"] = h[:W].tolist()
-            st.scratch["idx_out_splits"] = h[W:].tolist()
+            st.sc["idx_in_splits"] = h[:W].tolist()
+            st.sc["idx_out_splits"] = h[W:].tolist()
             self._pack_ids(st)
-        self.comm.all_to_all([st.scratch["recv_ids"] for st in S], [st.scratch["send_ids"] for st in S],
-                             [st.scratch["idx_out_splits"] for st in S], [st.scratch["idx_in_splits"] for st in S])
-        # ---- phase 3: permute + fused forward
+        self.comm.all_to_all([st.sc["recv_ids"] for st in S], [st.sc["send_ids"] for st in S],
+                             [st.sc["idx_out_splits"] for st in S], [st.sc["idx_in_splits"] for st in S])
+
+    def step(self, batches: Sequence, lr: float, eps: float = 0.0,
+             upstream_fn: Optional[Callable] = None, timers: Optional[dict] = None):
+        """One training step.  batches[i] = (lengths (T, B) int64 host array,
+        ids (table-major, device), optional lengths already on the device)
+        for local rank slot i.  Returns the pooled (B, sum D) outputs per
+        local rank (model table order).  upstream_fn(pooled) -> gradient
+        (default: ones, the reference's sum-of-outputs loss).  timers: dict
+        receiving CUDA event pairs for "fwd", "a2a_fwd", "a2a_bwd", "bwd"."""
+        W = self.W
+        S = self.states
+        ev = _Timers(timers)
+        self._exchange_inputs(batches)
+        ev.start("fwd")
         for st in S:
             self._forward_local(st)
-        self.comm.all_to_all([st.scratch["recv_pool"] for st in S], [st.scratch["send_pool"] for st in S],
-                             [st.scratch["pool_out_splits"] for st in S], [st.scratch["pool_in_splits"] for st in S])
-        pooled = []
-        for st in S:
-            pooled.append(self._assemble(st))
-        # ---- phase 4: upstream, backward exchange
+        ev.stop("fwd")
+        ev.start("a2a_fwd")
+        self.comm.all_to_all([st.sc["recv_pool"] for st in S], [st.sc["send_pool"] for st in S],
+                             [[self.B * wd for wd in self.widths] for st in S],
+                             [[self.B * self.widths[st.rank]] * W for st in S])
+        ev.stop("a2a_fwd")
+        pooled = [self._assemble(st) for st in S]
         for st, p in zip(S, pooled):
-            g = upstream_fn(p) if upstream_fn is not None else torch.ones_like(p)
+            if upstream_fn is not None:
+                g = upstream_fn(p)
+            else:
+                g = self._buf(st, "ones", p.numel(), p.dtype)[:p.numel()].view_as(p)
+                if not st.cache.get("ones_ready") is g.data_ptr():
+                    g.fill_(1.0)
+                    st.cache["ones_ready"] = g.data_ptr()
             self._pack_grad(st, g)
-        self.comm.all_to_all([st.scratch["recv_grad"] for st in S], [st.scratch["send_grad"] for st in S],
-                             [st.scratch["grad_out_splits"] for st in S], [st.scratch["grad_in_splits"] for st in S])
+        ev.start("a2a_bwd")
+        self.comm.all_to_all([st.sc["recv_grad"] for st in S], [st.sc["send_grad"] for st in S],
+                             [[self.B * self.widths[st.rank]] * W for st in S],
+                             [[self.B * wd for wd in self.widths] for st in S])
+        ev.stop("a2a_bwd")
+        ev.start("bwd")
         for st in S:
             self._backward_local(st, lr, eps)
-        if lay.dp_tables:
+        ev.stop("bwd")
+        if self.lay.dp_tables:
             self.comm.all_reduce_sum([st.dp_dense for st in S])
             for st in S:
                 self._dp_update(st, lr, eps)
         return pooled
 
     def redistribute(self, batches: Sequence) -> list:
-        """Run only the input exchange (phases 1-2 + permute) and return, per
-        local rank, {"shards": {(table, shard index): (lengths, ids)},
-        "dp": {table: (lengths, ids)}} as host arrays (comms.py:292-353)."""
-        lay, W, B = self.lay, self.W, self.B
-        S = self.states
-        for st, (lengths, ids) in zip(S, batches):
-            self._pack_lengths(st, np.asarray(lengths, dtype=np.int64), ids)
-        self.comm.all_to_all([st.scratch["recv_len"] for st in S], [st.scratch["send_len"] for st in S],
-                             [st.scratch["len_out_splits"] for st in S], [st.scratch["len_in_splits"] for st in S])
-        cnts = []
-        for st in S:
-            nS = len(lay.owned[st.rank])
-            recv = st.scratch["recv_len"].view(W, nS * B).sum(dim=1) if nS else \
-                torch.zeros(W, dtype=torch.int64, device=self.device)
-            cnts.append(torch.cat([st.scratch["send_counts"], recv]))
-        host = torch.stack(cnts).cpu().numpy()
-        for st, h in zip(S, host):
-            st.scratch["idx_in_splits"] = h[:W].tolist()
-            st.scratch["idx_out_splits"] = h[W:].tolist()
-            self._pack_ids(st)
-        self.comm.all_to_all([st.scratch["recv_ids"] for st in S], [st.scratch["send_ids"] for st in S],
-                             [st.scratch["idx_out_splits"] for st in S], [st.scratch["idx_in_splits"] for st in S])
+        """Run only the input exchange (+ permute) and return, per local rank,
+        {"shards": {(table, shard index): (lengths, ids)}, "dp": {table:
+        (lengths, ids)}} as host arrays (comms.py:292-353)."""
+        W, B = self.W, self.B
+        self._exchange_inputs(batches)
         res = []
-        for st, (lengths, _) in zip(S, batches):
-            sc = st.scratch
-            shards = lay.owned[st.rank]
+        for st, bt in zip(self.states, batches):
+            lengths = bt[0]
+            sc = st.sc
+            shards = self.lay.owned[st.rank]
             nS = len(shards)
             out = {"shards": {}, "dp": {}}
             if nS:
-                total = int(sum(sc["idx_out_splits"]))
-                rl = sc["recv_len"][:W * nS * B]
-                if total:
-                    pl, pi = tbe.permute_blocks(W, nS, B, rl, sc["recv_ids"][:total])
-                    pi = pi.cpu().numpy()
-                else:
-                    pl, _ = tbe.permute_blocks(W, nS, B, rl, torch.zeros(1, dtype=self.index_dtype, device=self.device))
-                    pi = np.zeros(0, dtype=np.int64)
+                pl, pi, _ = self._permute_local(st)
                 pl = pl.cpu().numpy().reshape(nS, W * B)
+                pi = pi.cpu().numpy()
                 pos = 0
                 for k, s in enumerate(shards):
                     c = int(pl[k].sum())
@@ -298,196 +317,206 @@ class ShardedEmbedding:
                     pos += c
             ids_h = sc["ids"].cpu().numpy()
             tab_off = sc["tab_off"]
-            for t in lay.dp_tables:
+            for t in self.lay.dp_tables:
                 out["dp"][t] = (np.asarray(lengths[t], dtype=np.int64).copy(),
                                 ids_h[int(tab_off[t]):int(tab_off[t + 1])].astype(np.int64))
             res.append(out)
         return res
 
     # -- phase helpers ---------------------------------------------------
-    def _pack_lengths(self, st: RankState, lengths: np.ndarray, ids: torch.Tensor) -> None:
+    def _pack_lengths(self, st: RankState, bt) -> None:
         lay, W, B, T = self.lay, self.W, self.B, self.T
         dev = self.device
+        lengths = np.asarray(bt[0], dtype=np.int64)
+        ids = bt[1]
         if lengths.shape != (T, B):
             raise LayoutMismatch(f"rank {st.rank}: lengths must be ({T}, {B})")
-        sc = st.scratch
-        ids = ids.to(dev)
         if int(ids.numel()) != int(lengths.sum()):
             raise LayoutMismatch("lengths do not cover the index buffer")
+        if ids.dtype != self.index_dtype:
+            raise LayoutMismatch("ids dtype must match the engine's index dtype")
+        sc = st.sc
+        ids = ids.to(dev)
         sc["ids"] = ids
         cnt = lengths.sum(axis=1)
         tab_off = np.concatenate(([0], np.cumsum(cnt)))
         sc["tab_off"] = tab_off
-        L_dev = torch.from_numpy(lengths.reshape(-1)).to(dev)
+        L_dev = bt[2] if len(bt) > 2 and bt[2] is not None else torch.from_numpy(lengths.reshape(-1)).to(dev)
         sc["L_dev"] = L_dev
         es = ids.element_size()
-        # row-wise tables: bucketise this rank's block once per table
         rw = {}
-        for t, bounds in lay.rw_bounds.items():
+        for t, bounds in lay.rw_bounds.items():  # bucketise this rank's block per row-wise table
             starts = [b[0] for b in bounds] + [bounds[-1][1]]
             sub = ids[int(tab_off[t]):int(tab_off[t + 1])]
-            off_t = tbe.lengths_to_offsets(L_dev[t * B:(t + 1) * B])
             if sub.numel() == 0:
                 sub = torch.zeros(1, dtype=ids.dtype, device=dev)
-            rw[t] = tbe.bucketize_rowwise(off_t, sub, starts)
+            rw[t] = tbe.bucketize_rowwise(tbe.lengths_to_offsets(L_dev[t * B:(t + 1) * B]), sub, starts)
         sc["rw"] = rw
-        # blocks in send order: destination-major, then the destination's shards
-        len_srcs, blk_ptr, blk_cnt, dest_of_blk = [], [], [], []
-        for v in range(W):
-            for s in lay.owned[v]:
-                if s.kind == "row_wise":
-                    j = lay.rw_bounds[s.table].index(s.rows)
-                    o_len, o_off, o_idx = rw[s.table]
-                    len_srcs.append(o_len[j])
-                    lo = o_off[j * B]
-                    blk_ptr.append(o_idx.data_ptr() + lo * es)
-                    blk_cnt.append(o_off[(j + 1) * B] - lo)
-                else:
-                    len_srcs.append(L_dev[s.table * B:(s.table + 1) * B])
-                    blk_ptr.append(ids.data_ptr() + int(tab_off[s.table]) * es)
-                    blk_cnt.append(int(cnt[s.table]))
-                dest_of_blk.append(v)
-        nsend = len(len_srcs)
-        send_len = torch.empty(max(nsend * B, 1), dtype=torch.int64, device=dev)
-        if nsend:
-            tbe.gather_blocks(len_srcs, [B] * nsend, send_len)
-        sc["send_len"] = send_len
-        sc["len_in_splits"] = [len(lay.owned[v]) * B for v in range(W)]
+        nb = len(self.send_blocks)
         nS = len(lay.owned[st.rank])
-        sc["recv_len"] = torch.empty(max(W * nS * B, 1), dtype=torch.int64, device=dev)
-        sc["len_out_splits"] = [nS * B] * W
-        # device block table for the id gather (counts of row-wise blocks live on the device)
-        if nsend:
-            cnt_dev = torch.stack([c if torch.is_tensor(c) else torch.tensor(c, device=dev) for c in blk_cnt])
-            ptr_dev = torch.stack([p if torch.is_tensor(p) else torch.tensor(p, device=dev) for p in blk_ptr])
-            dst_dev = torch.cumsum(cnt_dev, 0) - cnt_dev
-            dest = torch.tensor(dest_of_blk, device=dev)
-            send_counts = torch.zeros(W, dtype=torch.int64, device=dev).index_add_(0, dest, cnt_dev)
-        else:
-            cnt_dev = ptr_dev = dst_dev = None
-            send_counts = torch.zeros(W, dtype=torch.int64, device=dev)
+        sc["recv_len"] = self._buf(st, "recv_len", W * nS * B, torch.int64)
+        sc["send_len"] = self._buf(st, "send_len", nb * B, torch.int64)
+        if not nb:
+            sc["send_counts"] = torch.zeros(W, dtype=torch.int64, device=dev)
+            sc["blk"] = None
+            return
+        len_ptr = np.empty(nb, dtype=np.int64)
+        ptr = np.empty(nb, dtype=np.int64)
+        cnt_h = np.empty(nb, dtype=np.int64)
+        rw_pos, rw_ref = [], []
+        base_L = L_dev.data_ptr()
+        for i, (v, s) in enumerate(self.send_blocks):
+            if s.kind == "row_wise":
+                j = self.rw_slot[(s.table, s.index)]
+                o_len, o_off, o_idx = rw[s.table]
+                len_ptr[i] = o_len[j].data_ptr()
+                ptr[i] = o_idx.data_ptr()
+                cnt_h[i] = 0
+                rw_pos.append(i)
+                rw_ref.append((s.table, j))
+            else:
+                len_ptr[i] = base_L + s.table * B * 8
+                ptr[i] = ids.data_ptr() + int(tab_off[s.table]) * es
+                cnt_h[i] = int(cnt[s.table])
+        meta = torch.from_numpy(np.stack([len_ptr, np.full(nb, B, np.int64), np.arange(nb, dtype=np.int64) * B,
+                                          ptr, cnt_h])).to(dev, non_blocking=False)
+        tbe.gather_blocks_dev(meta[0], meta[1], meta[2], sc["send_len"])
+        ptr_dev, cnt_dev = meta[3].clone(), meta[4].clone()
+        if rw_pos:  # row-wise block sizes / starts live on the device
+            pos = torch.tensor(rw_pos, dtype=torch.int64, device=dev)
+            lo = torch.stack([rw[t][1][j * B] for t, j in rw_ref])
+            hi = torch.stack([rw[t][1][(j + 1) * B] for t, j in rw_ref])
+            ptr_dev.index_add_(0, pos, lo * es)
+            cnt_dev.index_copy_(0, pos, hi - lo)
+        dst_dev = torch.cumsum(cnt_dev, 0) - cnt_dev
+        dest = self._dest_index(st)
+        sc["send_counts"] = torch.zeros(W, dtype=torch.int64, device=dev).index_add_(0, dest, cnt_dev)
         sc["blk"] = (ptr_dev, cnt_dev, dst_dev)
-        sc["send_counts"] = send_counts
+
+    def _dest_index(self, st: RankState) -> torch.Tensor:
+        d = st.cache.get("dest")
+        if d is None:
+            d = torch.tensor([v for v, _ in self.send_blocks], dtype=torch.int64, device=self.device)
+            st.cache["dest"] = d
+        return d
 
     def _pack_ids(self, st: RankState) -> None:
-        sc = st.scratch
-        dev = self.device
+        sc = st.sc
         total_send = int(sum(sc["idx_in_splits"]))
         total_recv = int(sum(sc["idx_out_splits"]))
-        sc["send_ids"] = torch.empty(max(total_send, 1), dtype=self.index_dtype, device=dev)
-        sc["recv_ids"] = torch.empty(max(total_recv, 1), dtype=self.index_dtype, device=dev)
-        ptr, cnt, dst = sc["blk"]
-        if ptr is not None and total_send:
-            ids = sc["ids"]
-            if ids.dtype != self.index_dtype:
-                raise LayoutMismatch("ids dtype must match the engine's index dtype")
-            tbe.gather_blocks_dev(ptr, cnt, dst, sc["send_ids"])
+        sc["send_ids"] = self._buf(st, "send_ids", total_send, self.index_dtype)
+        sc["recv_ids"] = self._buf(st, "recv_ids", total_recv, self.index_dtype)
+        if sc["blk"] is not None and total_send:
+            tbe.gather_blocks_dev(*sc["blk"], sc["send_ids"])
+
+    def _permute_local(self, st: RankState):
+        """(W, S, B) received blocks -> (S, W, B): each local shard sees the
+        global batch in sample order (comms.py:248-252)."""
+        W, B = self.W, self.B
+        sc = st.sc
+        nS = len(self.lay.owned[st.rank])
+        total = int(sum(sc["idx_out_splits"]))
+        rl = sc["recv_len"][:W * nS * B]
+        ri = sc["recv_ids"][:max(total, 1)]
+        perm_len = self._buf(st, "perm_len", W * nS * B, torch.int64)[:W * nS * B]
+        perm_ids = self._buf(st, "perm_ids", total, self.index_dtype)[:max(total, 1)]
+        ws_bytes = tbe.capi.lib().neo_permute_workspace_bytes(W, nS)
+        ws = tbe.WORKSPACE.get("permute", ws_bytes, self.device)
+        tbe.capi.check(tbe.capi.lib().neo_permute_blocks(
+            W, nS, B, rl.data_ptr(), ri.data_ptr(), tbe.INDEX_CODE[self.index_dtype], perm_len.data_ptr(),
+            perm_ids.data_ptr(), ws.data_ptr(), ws.numel(), tbe._stream()), "neo_permute_blocks")
+        off = tbe.lengths_to_offsets(perm_len)
+        return perm_len, perm_ids, off
 
     def _forward_local(self, st: RankState) -> None:
-        lay, W, B, n = self.lay, self.W, self.B, self.n
-        sc = st.scratch
-        dev = self.device
-        shards = lay.owned[st.rank]
-        nS = len(shards)
-        width = lay.width(st.rank)
-        sc["send_pool"] = torch.empty(max(n * width, 1), dtype=self.fwd_comm, device=dev)
-        if nS:
-            # (W, S, B) wire blocks -> (S, W, B): each shard sees the global batch in sample order
-            total = int(sum(sc["idx_out_splits"]))
-            rl = sc["recv_len"][:W * nS * B]
-            ri = sc["recv_ids"][:max(total, 1)]
-            if total == 0:
-                perm_len, _ = tbe.permute_blocks(W, nS, B, rl, torch.zeros(1, dtype=self.index_dtype, device=dev))
-                perm_ids = ri
-            else:
-                perm_len, perm_ids = tbe.permute_blocks(W, nS, B, rl, ri)
-            off = tbe.lengths_to_offsets(perm_len)
+        W, B, n = self.W, self.B, self.n
+        sc = st.sc
+        width = self.widths[st.rank]
+        sc["send_pool"] = self._buf(st, "send_pool", n * width, self.fwd_comm)
+        sc["recv_pool"] = self._buf(st, "recv_pool", B * sum(self.widths), self.fwd_comm)
+        if st.group is not None:
+            _, perm_ids, off = self._permute_local(st)
             sc["perm_ids"], sc["perm_off"] = perm_ids, off
-            out = sc["send_pool"][:n * width].view(n, width)
-            st.group.forward(perm_ids, off, n, out=out)
-        sc["pool_in_splits"] = [B * width] * W
-        widths = [lay.width(w) for w in range(W)]
-        sc["pool_out_splits"] = [B * wd for wd in widths]
-        sc["recv_pool"] = torch.empty(max(B * sum(widths), 1), dtype=self.fwd_comm, device=dev)
-        # data-parallel tables: local batch only
-        if st.dp_group is not None:
+            st.group.forward(perm_ids, off, n, out=sc["send_pool"][:n * width].view(n, width))
+        if st.dp_group is not None:  # data-parallel tables: local batch only
             ids, tab_off, L_dev = sc["ids"], sc["tab_off"], sc["L_dev"]
-            dp = lay.dp_tables
+            dp = self.lay.dp_tables
             cnts = [int(tab_off[t + 1] - tab_off[t]) for t in dp]
-            dp_ids = torch.empty(max(sum(cnts), 1), dtype=ids.dtype, device=dev)
+            dp_ids = self._buf(st, "dp_ids", sum(cnts), ids.dtype)
             tbe.gather_blocks([ids[int(tab_off[t]):] if cnts[i] else ids for i, t in enumerate(dp)], cnts, dp_ids)
-            dp_len = torch.empty(len(dp) * B, dtype=torch.int64, device=dev)
+            dp_len = self._buf(st, "dp_len", len(dp) * B, torch.int64)[:len(dp) * B]
             tbe.gather_blocks([L_dev[t * B:(t + 1) * B] for t in dp], [B] * len(dp), dp_len)
-            dp_off = tbe.lengths_to_offsets(dp_len)
-            sc["dp_ids"], sc["dp_off"] = dp_ids, dp_off
-            sc["dp_out"] = st.dp_group.forward(dp_ids, dp_off, B, out_dtype=self.acc)
+            sc["dp_ids"], sc["dp_off"] = dp_ids, tbe.lengths_to_offsets(dp_len)
+            dp_out = self._buf(st, "dp_out", B * self.dp_width, self.acc)[:B * self.dp_width].view(B, self.dp_width)
+            sc["dp_out"] = st.dp_group.forward(dp_ids, sc["dp_off"], B, out=dp_out)
 
     def _assemble(self, st: RankState) -> torch.Tensor:
         """Place received column blocks (TW copy, CW column placement, RW
-        partial sum in shard order: comms.py:692-711) into model order."""
+        partial sums in shard order: comms.py:692-711) in model order."""
         lay, W, B = self.lay, self.W, self.B
-        sc = st.scratch
-        dev = self.device
-        pooled = torch.empty((B, lay.total_dim), dtype=self.acc, device=dev)
-        widths = [lay.width(w) for w in range(W)]
-        starts = np.concatenate(([0], np.cumsum([B * wd for wd in widths])))
-        views = [sc["recv_pool"][int(starts[w]):int(starts[w + 1])].view(B, widths[w]) if widths[w] else None
-                 for w in range(W)]
-        where = {}
-        for w in range(W):
-            for s in lay.owned[w]:
-                where[(s.table, s.index)] = (w, s)
-        pieces, dp_pieces = [], []
-        dp_col = {t: c for t, c in zip(lay.dp_tables, np.concatenate(([0], np.cumsum([lay.dims[t] for t in lay.dp_tables])))[:-1])}
-        for t in range(self.T):
-            if t in dp_col:
-                dp_pieces.append(tbe.Piece(sc["dp_out"], pooled, int(dp_col[t]), lay.model_cols[t], lay.dims[t]))
-                continue
-            idxs = sorted(i for (tt, i) in where if tt == t)
-            for n_i, i in enumerate(idxs):
-                w, s = where[(t, i)]
-                acc = s.kind == "row_wise" and n_i > 0
-                pieces.append(tbe.Piece(views[w], pooled, s.out_col, lay.model_cols[t] + s.cols[0], s.dim, acc))
-        tbe.copy_pieces(B, pieces)
-        tbe.copy_pieces(B, dp_pieces)
+        sc = st.sc
+        pooled = self._buf(st, "pooled", B * lay.total_dim, self.acc)[:B * lay.total_dim].view(B, lay.total_dim)
+        key = ("asm", sc["recv_pool"].data_ptr(), pooled.data_ptr(),
+               sc["dp_out"].data_ptr() if "dp_out" in sc else 0)
+        packed = st.cache.get(key)
+        if packed is None:
+            starts = np.concatenate(([0], np.cumsum([B * wd for wd in self.widths])))
+            views = [sc["recv_pool"][int(starts[w]):int(starts[w + 1])].view(B, self.widths[w])
+                     if self.widths[w] else None for w in range(W)]
+            where = {(s.table, s.index): (w, s) for w in range(W) for s in lay.owned[w]}
+            pieces, dp_pieces = [], []
+            for t in range(self.T):
+                if t in self.dp_cols:
+                    dp_pieces.append(tbe.Piece(sc["dp_out"], pooled, self.dp_cols[t], lay.model_cols[t], lay.dims[t]))
+                    continue
+                for k, i in enumerate(sorted(i for (tt, i) in where if tt == t)):
+                    w, s = where[(t, i)]
+                    pieces.append(tbe.Piece(views[w], pooled, s.out_col, lay.model_cols[t] + s.cols[0], s.dim,
+                                            s.kind == "row_wise" and k > 0))
+            packed = [(pl, tbe.pack_pieces(pl, self.device) if pl else None) for pl in (pieces, dp_pieces)]
+            st.cache[key] = packed
+        for pl, dev_tab in packed:
+            if pl:
+                tbe.copy_pieces(B, pl, dev_tab)
         return pooled
 
     def _pack_grad(self, st: RankState, grad: torch.Tensor) -> None:
         lay, W, B = self.lay, self.W, self.B
-        sc = st.scratch
-        dev = self.device
+        sc = st.sc
         grad = grad.contiguous()
-        widths = [lay.width(v) for v in range(W)]
-        send = torch.empty(max(B * sum(widths), 1), dtype=self.bwd_comm, device=dev)
-        starts = np.concatenate(([0], np.cumsum([B * wd for wd in widths])))
-        pieces = []
-        for v in range(W):
-            if not widths[v]:
-                continue
-            chunk = send[int(starts[v]):int(starts[v + 1])].view(B, widths[v])
-            for s in lay.owned[v]:
-                pieces.append(tbe.Piece(grad, chunk, lay.model_cols[s.table] + s.cols[0], s.out_col, s.dim))
-        tbe.copy_pieces(B, pieces)
+        send = self._buf(st, "send_grad", B * sum(self.widths), self.bwd_comm)
+        me = self.widths[st.rank]
         sc["send_grad"] = send
-        sc["grad_in_splits"] = [B * wd for wd in widths]
-        me = lay.width(st.rank)
-        sc["grad_out_splits"] = [B * me] * W
-        sc["recv_grad"] = torch.empty(max(self.n * me, 1), dtype=self.bwd_comm, device=dev)
+        sc["recv_grad"] = self._buf(st, "recv_grad", self.n * me, self.bwd_comm)
+        g_dp = None
         if st.dp_group is not None:
-            dpw = sum(lay.dims[t] for t in lay.dp_tables)
-            g_dp = torch.empty((B, dpw), dtype=self.acc, device=dev)
-            c = 0
-            dp_pieces = []
-            for t in lay.dp_tables:
-                dp_pieces.append(tbe.Piece(grad, g_dp, lay.model_cols[t], c, lay.dims[t]))
-                c += lay.dims[t]
-            tbe.copy_pieces(B, dp_pieces)
+            g_dp = self._buf(st, "dp_grad", B * self.dp_width, self.acc)[:B * self.dp_width].view(B, self.dp_width)
             sc["dp_grad"] = g_dp
+        key = ("grad", grad.data_ptr(), send.data_ptr(), 0 if g_dp is None else g_dp.data_ptr())
+        packed = st.cache.get(key)
+        if packed is None:
+            starts = np.concatenate(([0], np.cumsum([B * wd for wd in self.widths])))
+            pieces = []
+            for v in range(W):
+                if not self.widths[v]:
+                    continue
+                chunk = send[int(starts[v]):int(starts[v + 1])].view(B, self.widths[v])
+                for s in lay.owned[v]:
+                    pieces.append(tbe.Piece(grad, chunk, lay.model_cols[s.table] + s.cols[0], s.out_col, s.dim))
+            dp_pieces = [tbe.Piece(grad, g_dp, lay.model_cols[t], self.dp_cols[t], lay.dims[t])
+                         for t in lay.dp_tables] if g_dp is not None else []
+            packed = [(pl, tbe.pack_pieces(pl, self.device) if pl else None) for pl in (pieces, dp_pieces)]
+            if len(st.cache) > 64:
+                st.cache.clear()
+            st.cache[key] = packed
+        for pl, dev_tab in packed:
+            if pl:
+                tbe.copy_pieces(B, pl, dev_tab)
 
     def _backward_local(self, st: RankState, lr: float, eps: float) -> None:
-        sc = st.scratch
-        if st.group is not None and "perm_ids" in sc:
-            me = self.lay.width(st.rank)
+        sc = st.sc
+        if st.group is not None:
+            me = self.widths[st.rank]
             g = sc["recv_grad"][:self.n * me].view(self.n, me)
             st.group.backward(sc["perm_ids"], sc["perm_off"], self.n, g, mode="update", optim=self.optim,
                               lr=lr, eps=eps)
@@ -504,7 +533,25 @@ class ShardedEmbedding:
     def shard_tensors(self, rank_slot: int = 0):
         """[(LocalShard, weight, moment)] of a local rank."""
         st = self.states[rank_slot]
-        shards = self.lay.owned[st.rank]
         if st.group is None:
             return []
-        return list(zip(shards, st.group.weights, st.group.moments))
+        return list(zip(self.lay.owned[st.rank], st.group.weights, st.group.moments))
+
+
+class _Timers:
+    """CUDA event pairs per phase on the current stream (no-op if unused)."""
+
+    def __init__(self, d: Optional[dict]):
+        self.d = d
+
+    def start(self, name: str) -> None:
+        if self.d is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.d.setdefault(name, []).append([e, None])
+
+    def stop(self, name: str) -> None:
+        if self.d is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.d[name][-1][1] = e
