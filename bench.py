@@ -9,7 +9,7 @@ all tables + one fused backward/row-wise-AdaGrad over all tables.
 
 N>1 (torchrun, one rank per GPU, NCCL): the sharded embedding step with the
 same per-GPU work (weak scaling): the 64 tables are placed table-wise by the
-reference planner's plan (tests/golden/plans), global batch 65,536 x N, and
+reference planner's plan (configs/plans), global batch 65,536 x N, and
 pooled rows / their gradients move through the all-to-all.
 
 --impl reference times the reference's CPU implementation of the same step
@@ -272,9 +272,7 @@ def run_b200(a, rank, world):
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     if world > 1:
-        from paper_2104_05158_b200 import dist as ndist
-
-        return ndist.bench_sharded(a, rank, world, dev)
+        return run_sharded(a, rank, world, dev)
     T, H, D, B, L = a.tables, a.rows, a.dim, a.batch, a.pooling
     N = B * L
     torch.manual_seed(0)
@@ -372,6 +370,155 @@ def e2e_b200(a, grp, dev) -> dict:
             "h2d_bytes_per_step": host[0].numel() * 4 + lengths.numel() * 8, "d2h_bytes_per_step": 8,
             "api": "paper_2104_05158_b200.pipeline.TrainPipeline.run (pinned host ids/lengths, "
                    "H2D prefetch overlapped with the previous step, loss = sum of pooled outputs read back)"}
+
+
+def expected_unique(H: int, N: int) -> float:
+    return H * (1.0 - (1.0 - 1.0 / H) ** N)
+
+
+def run_sharded(a, rank, world, dev):
+    """N>1: sharded embedding step over NCCL, weak scaling (B per GPU fixed)."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2104_05158_b200 import dist as nd
+    from paper_2104_05158_b200 import plan as P
+    from paper_2104_05158_b200 import spec
+
+    tdist.init_process_group("nccl", device_id=dev)
+    T, H, D, B, L = a.tables, a.rows, a.dim, a.batch, a.pooling
+    plan_file = ROOT / "configs" / "plans" / f"c2_w{world}.json"
+    plan = P.plan_from_json(plan_file.read_text())
+    model = spec.ModelSpec(tables=tuple(spec.TableSpec(f"t{i}", H, D, float(L)) for i in range(T)), local_batch=B)
+    comm = nd.NcclComm()
+    eng = nd.ShardedEmbedding(model, plan, comm, B, device=dev, dtype=torch.float32, optim="rowwise_adagrad",
+                              index_dtype=torch.int32)
+    torch.manual_seed(rank)
+    for st in eng.states:
+        if st.group is not None:
+            st.group._storage.normal_()
+    lengths = np.full((T, B), L, dtype=np.int64)
+    L_dev = torch.full((T * B,), L, dtype=torch.int64, device=dev)
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    ids = [torch.randint(0, H, (T * B * L,), dtype=torch.int32, device=dev, generator=g) for _ in range(2)]
+
+    def step(i, timers=None):
+        return eng.step([(lengths, ids[i % 2], L_dev)], lr=LR, eps=EPS, timers=timers)
+
+    for i in range(a.warmup):
+        step(i)
+    launches_per_step = count_launches(lambda: step(0))
+    torch.cuda.synchronize()
+    tdist.barrier()
+    clocks = Clocks(dev.index) if rank == 0 else None
+    time.sleep(0.3)
+    timers = {}
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(a.steps):
+        step(i, timers)
+    e1.record()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms_local = e0.elapsed_time(e1) / a.steps
+    ph = {k: float(np.mean([x.elapsed_time(y) for x, y in v])) for k, v in timers.items()}
+    t = torch.tensor([ms_local, ph.get("fwd", 0.0), ph.get("bwd", 0.0), ph.get("a2a_fwd", 0.0),
+                      ph.get("a2a_bwd", 0.0)], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms, fwd_ms, bwd_ms, a2f_ms, a2b_ms = t.tolist()
+    # per-rank algorithmic bytes of the local TBE (max over ranks of local tables)
+    T_loc = max(len(eng.lay.owned[v]) for v in range(world))
+    n = B * world
+    N = n * L
+    U = expected_unique(H, N)
+    fb = fwd_bytes(T_loc, N, D, n)
+    bb = bwd_bytes([U] * T_loc, N, D, n)
+    peak, peak_kind = hbm_peak()
+    send = max(eng.pooled_send_bytes(v) for v in range(world))
+    e2e = None if a.no_e2e else e2e_sharded(a, eng, rank, world, dev, lengths, L_dev)
+    if rank != 0:
+        tdist.destroy_process_group()
+        return
+    fwd_gbs = fb / (fwd_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": B * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(a) + f", sharded over {world} GPUs ({plan_file.name}: reference "
+                   "plan_4d, table-wise)", "tables": T, "rows": H, "dim": D, "batch_per_gpu": B,
+                   "global_batch": B * world, "pooling": L, "parallelism": f"tw{world}",
+                   "l2": "inputs larger than L2"},
+        "roofline": {"bound": "hbm", "kernel": "tbe_forward_kernel (local shards)", "achieved": fwd_gbs, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak, "traffic": None,
+                     "algorithmic_bytes": fb, "ms": fwd_ms},
+        "phases_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "a2a_fwd": a2f_ms, "a2a_bwd": a2b_ms},
+        "alltoall": {"send_bytes_per_gpu": send, "fwd_busbw_gbs": send / (a2f_ms * 1e-3) / 1e9,
+                     "bwd_busbw_gbs": send / (a2b_ms * 1e-3) / 1e9, "peak_gbs": 900.0,
+                     "note": "per-GPU send bytes excluding self (comms.py:366-392) / all_to_all time"},
+        "roofline_bwd": {"achieved": bb / (bwd_ms * 1e-3) / 1e9, "bytes_expected_U": bb, "ms": bwd_ms},
+        "gpu_launches": launches_per_step * a.steps,
+        "clocks": clk,
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
+
+
+def e2e_sharded(a, eng, rank, world, dev, lengths, L_dev) -> dict:
+    """Sharded step with host (pinned) ids copied H2D each step on a side
+    stream (prefetch of the next batch overlaps the current step) and the
+    loss read back D2H."""
+    import torch
+    import torch.distributed as tdist
+
+    T, H, B, L = a.tables, a.rows, a.batch, a.pooling
+    gen = torch.Generator().manual_seed(99 + rank)
+    host = [torch.randint(0, H, (T * B * L,), dtype=torch.int32, generator=gen).pin_memory() for _ in range(2)]
+    dev_ids = [torch.empty_like(h, device=dev) for h in host]
+    copied = [torch.cuda.Event() for _ in range(2)]
+    free = [torch.cuda.Event() for _ in range(2)]
+    cs = torch.cuda.Stream(device=dev)
+    comp = torch.cuda.current_stream(dev)
+    losses = torch.empty(a.warmup + a.steps, dtype=torch.float32, pin_memory=True)
+
+    def stage(i):
+        with torch.cuda.stream(cs):
+            cs.wait_event(free[i % 2])
+            dev_ids[i % 2].copy_(host[i % 2], non_blocking=True)
+            copied[i % 2].record(cs)
+
+    for e in free:
+        e.record(comp)
+    total = a.warmup + a.steps
+    stage(0)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    for i in range(total):
+        if i == a.warmup:
+            torch.cuda.synchronize()
+            tdist.barrier()
+            e0.record(comp)
+        if i + 1 < total:
+            stage(i + 1)
+        comp.wait_event(copied[i % 2])
+        pooled = eng.step([(lengths, dev_ids[i % 2], L_dev)], lr=LR, eps=EPS)
+        losses[i:i + 1].copy_(pooled[0].sum().reshape(1), non_blocking=True)
+        free[i % 2].record(comp)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / a.steps], dtype=torch.float64, device=dev)
+    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    ms = float(ms.item())
+    return {"value": B * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+            "h2d_bytes_per_step": host[0].numel() * 4 * world + lengths.size * 8 * world,
+            "d2h_bytes_per_step": 4 * world,
+            "api": "paper_2104_05158_b200.dist.ShardedEmbedding.step (pinned host ids per rank, H2D prefetch "
+                   "overlapped, loss read back)"}
 
 
 def main(argv=None):

@@ -284,6 +284,58 @@ struct alignas(16) StreamSmem {
   int32_t ent[kGRing];            // (head << 16) | seg slot
 };
 
+// Lane-parallel metadata of a 32-entry window: lane l describes entry base+l.
+template <typename W, typename G>
+struct Window {
+  int64_t base;
+  uint64_t key;
+  unsigned heads;   // bit l: entry base+l starts a segment
+  unsigned live;    // bit l: entry is a valid row id (< total_rows, < N)
+  uint64_t gptr;    // upstream row of this lane's entry (table column offset applied)
+  uint64_t wptr;    // weight row
+  uint64_t mptr;    // moment (row-wise scalar / element-wise row)
+  int32_t D;        // table dim of this lane's entry
+  int32_t vec;      // 16-byte vector path usable for this entry's table
+};
+
+template <typename W, typename G, typename Key>
+__device__ __forceinline__ void load_window(const SegParams& p, int64_t base, uint64_t prev_key, int lane,
+                                            Window<W, G>& w) {
+  constexpr int kVec = 16 / sizeof(W);
+  const unsigned full = 0xffffffffu;
+  const Key* keys = reinterpret_cast<const Key*>(p.keys);
+  const int64_t j = base + lane;
+  w.base = base;
+  const bool in = j < p.N;
+  w.key = in ? (uint64_t)keys[j] : ~0ull;
+  const int32_t bag = in ? p.bags[j] : 0;
+  uint64_t pv = __shfl_up_sync(full, w.key, 1);
+  if (lane == 0) pv = prev_key;
+  w.heads = __ballot_sync(full, w.key != pv);
+  const bool ok = in && w.key < (uint64_t)p.total_rows;
+  w.live = __ballot_sync(full, ok);
+  w.gptr = w.wptr = w.mptr = 0;
+  w.D = 0;
+  w.vec = 0;
+  if (ok) {
+    const int32_t t = bag / (int32_t)p.B;
+    const int64_t row = (int64_t)w.key - p.row_offsets[t];
+    const int32_t doff = p.dim_offsets[t];
+    const int32_t D = p.dim_offsets[t + 1] - doff;
+    const G* grad = reinterpret_cast<const G*>(p.grad);
+    const W* wbase = reinterpret_cast<const W*>(p.weights[t]);
+    w.D = D;
+    w.vec = (D % kVec) == 0 && aligned16(wbase) && (doff % kVec) == 0 && (p.grad_stride % kVec) == 0 &&
+            (reinterpret_cast<uintptr_t>(grad) % min(16, (int)(sizeof(G) * kVec))) == 0;
+    w.gptr = reinterpret_cast<uint64_t>(grad + ((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + doff);
+    w.wptr = reinterpret_cast<uint64_t>(wbase + row * D);
+    float* mb = p.moments ? reinterpret_cast<float*>(p.moments[t]) : nullptr;
+    w.mptr = reinterpret_cast<uint64_t>(p.optim == NEO_OPT_ROWWISE_ADAGRAD ? mb + row
+                                        : p.optim == NEO_OPT_ADAGRAD    ? mb + row * D
+                                                                        : nullptr);
+  }
+}
+
 template <typename W, typename G, typename Key>
 __global__ void __launch_bounds__(kStreamWarps * kWarp)
 tbe_stream_update_kernel(SegParams p) {
@@ -295,72 +347,47 @@ tbe_stream_update_kernel(SegParams p) {
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
   SM& sm = reinterpret_cast<SM*>(smem_raw)[warp];
   const Key* keys = reinterpret_cast<const Key*>(p.keys);
-  const int32_t* bags = p.bags;
-  const G* grad = reinterpret_cast<const G*>(p.grad);
   const int64_t N = p.N;
-  const uint64_t total = (uint64_t)p.total_rows;
   const int64_t nchunks = (N + kWarp - 1) / kWarp;
   const int64_t nwarps = (int64_t)gridDim.x * kStreamWarps;
   const float lr = (float)p.lr, eps = (float)p.eps;
   const int optim = p.optim;
-  const bool gvec_ok = (p.grad_stride % kVec) == 0 &&
-                       (reinterpret_cast<uintptr_t>(grad) % (kGB < 16 ? kGB : 16)) == 0;
 
   for (int64_t chunk = (int64_t)blockIdx.x * kStreamWarps + warp; chunk < nchunks; chunk += nwarps) {
     const int64_t c0 = chunk * kWarp;
-    // window of 32 entries for the producer
-    int64_t wbase = c0;
-    uint64_t wkey = c0 + lane < N ? (uint64_t)keys[c0 + lane] : ~0ull;
-    int32_t wbag = c0 + lane < N ? bags[c0 + lane] : 0;
-    uint64_t prev = __shfl_up_sync(full, wkey, 1);
-    if (lane == 0) prev = c0 > 0 ? (uint64_t)keys[c0 - 1] : ~wkey;
-    unsigned wbnd = __ballot_sync(full, wkey != prev);
-    if (wbnd == 0) continue;
-    const int64_t e_begin = c0 + (__ffs(wbnd) - 1);
-    if (__shfl_sync(full, wkey, __ffs(wbnd) - 1) >= total) continue;  // only invalid ids here
-
-    // producer state
-    int64_t pe = e_begin;
-    bool done = false;
-    int64_t e_end = -1;
+    Window<W, G> pw;  // producer window: the chunk, then (for the last segment) its continuation
+    load_window<W, G, Key>(p, c0, c0 > 0 ? (uint64_t)keys[c0 - 1] : ~0ull, lane, pw);
+    if (pw.heads == 0) continue;  // chunk lies inside a segment started earlier
+    const int e0 = __ffs(pw.heads) - 1;
+    if (!((pw.live >> e0) & 1u)) continue;  // only invalid ids (they sort last)
+    // producer cursor (offset from c0): runs kLead entries ahead of the consumer
+    int pe = e0;
+    int pend = -1;  // range end once known: first head at/after c0+32, first invalid entry, or N
     int wslot = -1;
-    int32_t pt = 0, pdoff = 0, pD = 0;
-    bool pgvec = false;
+    int pD = 0, pvec = 0;
 
     auto produce = [&]() {
-      if (!done) {
-        if (pe - wbase >= kWarp) {  // slide the window
-          const uint64_t last = __shfl_sync(full, wkey, kWarp - 1);
-          wbase += kWarp;
-          wkey = wbase + lane < N ? (uint64_t)keys[wbase + lane] : ~0ull;
-          wbag = wbase + lane < N ? bags[wbase + lane] : 0;
-          uint64_t pv = __shfl_up_sync(full, wkey, 1);
-          if (lane == 0) pv = last;
-          wbnd = __ballot_sync(full, wkey != pv);
+      if (pend < 0) {
+        int l = pe - (int)(pw.base - c0);
+        if (l == kWarp) {  // slide into the next window (continuation of the last segment)
+          const uint64_t last = __shfl_sync(full, pw.key, kWarp - 1);
+          load_window<W, G, Key>(p, pw.base + kWarp, last, lane, pw);
+          l = 0;
         }
-        const int l = (int)(pe - wbase);
-        const bool head = (wbnd >> l) & 1u;
-        const uint64_t k = __shfl_sync(full, wkey, l);
-        const int32_t bag = __shfl_sync(full, wbag, l);
-        if (pe >= N || k >= total || (head && pe >= c0 + kWarp)) {
-          done = true;
-          e_end = pe;
+        const bool head = (pw.heads >> l) & 1u;
+        const bool live = (pw.live >> l) & 1u;
+        if (!live || (head && pe >= kWarp)) {
+          pend = pe;
         } else {
+          const uint64_t gp = __shfl_sync(full, pw.gptr, l);
           if (head) {  // new segment: stage its weight row + moment
             wslot = wslot + 1 == kWRing ? 0 : wslot + 1;
-            pt = bag / (int32_t)p.B;
-            const int64_t row = (int64_t)k - p.row_offsets[pt];
-            pdoff = p.dim_offsets[pt];
-            pD = p.dim_offsets[pt + 1] - pdoff;
-            W* wrow = reinterpret_cast<W*>(p.weights[pt]) + row * pD;
-            float* mbase = p.moments ? reinterpret_cast<float*>(p.moments[pt]) : nullptr;
-            float* mptr = optim == NEO_OPT_ROWWISE_ADAGRAD ? mbase + row
-                          : optim == NEO_OPT_ADAGRAD      ? mbase + row * pD
-                                                          : nullptr;
-            const bool wvec = (pD % kVec) == 0 && aligned16(reinterpret_cast<const void*>(p.weights[pt]));
-            pgvec = wvec && gvec_ok && (pdoff % kVec) == 0;
-            const bool vec = wvec && pgvec;
-            if (vec) {
+            const uint64_t wp = __shfl_sync(full, pw.wptr, l);
+            const uint64_t mp = __shfl_sync(full, pw.mptr, l);
+            pD = __shfl_sync(full, pw.D, l);
+            pvec = __shfl_sync(full, pw.vec, l);
+            const W* wrow = reinterpret_cast<const W*>(wp);
+            if (pvec) {
               if (lane * kVec < pD) cp_async(&sm.w[wslot][lane][0], wrow + lane * kVec, 16);
             } else {  // unaligned table: synchronous strided staging
               W* ws = reinterpret_cast<W*>(&sm.w[wslot][lane][0]);
@@ -371,15 +398,13 @@ tbe_stream_update_kernel(SegParams p) {
               }
             }
             if (lane == 0) {
-              if (optim == NEO_OPT_ROWWISE_ADAGRAD) cp_async(&sm.mr[wslot], mptr, 4);
-              sm.seg[wslot] = SegMeta{reinterpret_cast<uint64_t>(wrow), reinterpret_cast<uint64_t>(mptr), pD,
-                                      vec ? 1 : 0};
+              if (optim == NEO_OPT_ROWWISE_ADAGRAD) cp_async(&sm.mr[wslot], reinterpret_cast<const float*>(mp), 4);
+              sm.seg[wslot] = SegMeta{wp, mp, pD, pvec};
             }
-            pgvec = vec;
           }
-          const int gs = (int)(pe % kGRing);
-          const G* grow = grad + ((int64_t)bag - (int64_t)pt * p.B) * p.grad_stride + pdoff;
-          if (pgvec) {
+          const int gs = pe & (kGRing - 1);
+          const G* grow = reinterpret_cast<const G*>(gp);
+          if (pvec) {
             if (lane * kVec < pD) {
               if constexpr (kGB == 32) {
                 cp_async(&sm.g[gs][lane][0], grow + lane * kVec, 16);
@@ -408,7 +433,7 @@ tbe_stream_update_kernel(SegParams p) {
     for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
     int cur = -1;
 
-    auto finalize = [&](int slot) {
+    auto finalize = [&](int slot) {  // one optimizer step (embedding.py:212-254)
       const SegMeta sg = sm.seg[slot];
       bool nz = false;
       float ss = 0.f;
@@ -417,8 +442,7 @@ tbe_stream_update_kernel(SegParams p) {
         nz |= acc[e] != 0.f;
         ss += acc[e] * acc[e];
       }
-      const bool any_nz = __any_sync(full, nz);
-      if (optim == NEO_OPT_SGD || any_nz) {
+      if (optim == NEO_OPT_SGD || __any_sync(full, nz)) {
         float denom = 1.f;
         if (optim == NEO_OPT_ROWWISE_ADAGRAD) {
           ss = warp_sum(ss);
@@ -426,6 +450,7 @@ tbe_stream_update_kernel(SegParams p) {
           if (lane == 0) *reinterpret_cast<float*>(sg.m) = m;
           denom = sqrtf(m) + eps;
         }
+        const float step_scale = lr / denom;
         const W* wsm = reinterpret_cast<const W*>(&sm.w[slot][lane][0]);
         W out[kVec];
         float mo[kVec];
@@ -433,15 +458,15 @@ tbe_stream_update_kernel(SegParams p) {
         for (int e = 0; e < kVec; ++e) {
           const float w = Elem<W>::to_f(wsm[e]);
           float r;
-          if (optim == NEO_OPT_SGD) {
-            r = w - lr * acc[e];
-          } else if (optim == NEO_OPT_ROWWISE_ADAGRAD) {
-            r = w - lr * acc[e] / denom;
-          } else {  // element-wise state read here (not staged: off the benchmark path)
+          if (optim == NEO_OPT_ADAGRAD) {  // element-wise state read here (not staged)
             const int j = sg.vec ? lane * kVec + e : lane + e * kWarp;
             const float mj = (j < sg.D ? reinterpret_cast<const float*>(sg.m)[j] : 0.f) + acc[e] * acc[e];
             mo[e] = mj;
             r = w - lr * acc[e] / (sqrtf(mj) + eps);
+          } else if (optim == NEO_OPT_ROWWISE_ADAGRAD) {
+            r = w - acc[e] * step_scale;
+          } else {
+            r = w - lr * acc[e];
           }
           out[e] = Elem<W>::from_f(r);
         }
@@ -473,26 +498,23 @@ tbe_stream_update_kernel(SegParams p) {
       for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
     };
 
+#pragma unroll 1
     for (int i = 0; i < kLead; ++i) produce();  // fill the pipeline
-    for (int64_t ce = e_begin;; ++ce) {
+#pragma unroll 1
+    for (int ce = e0;; ++ce) {
       produce();
-      if (done && ce >= e_end) break;
+      if (pend >= 0 && ce >= pend) break;
       cp_wait<kLead>();
       __syncwarp();
-      const int gs = (int)(ce % kGRing);
+      const int gs = ce & (kGRing - 1);
       const int ent = sm.ent[gs];
       if (ent >> 16) {
         if (cur >= 0) finalize(cur);
         cur = ent & 0xffff;
       }
-      const SegMeta& sg = sm.seg[cur];
       const G* gsm = reinterpret_cast<const G*>(&sm.g[gs][lane][0]);
-      const bool live = sg.vec ? lane * kVec < sg.D : true;
-      if (live) {
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
-      }
-      __syncwarp();
+      for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
     }
     if (cur >= 0) finalize(cur);
     cp_wait<0>();
