@@ -266,12 +266,6 @@ __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_grou
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-struct SegMeta {   // written by lane 0 of the producer, read by the consumer
-  uint64_t w;      // weight row pointer
-  uint64_t m;      // moment pointer (row-wise scalar or element-wise row)
-  int32_t D;
-  int32_t vec;     // 1: lane owns columns [lane*VEC, +VEC); 0: lane + e*32
-};
 
 template <typename W, typename G>
 struct alignas(16) StreamSmem {
@@ -280,12 +274,9 @@ struct alignas(16) StreamSmem {
   unsigned char g[kGRing][kWarp][kGBytes];
   unsigned char w[kWRing][kWarp][16];
   float mr[kWRing];               // row-wise moment
-  SegMeta seg[kWRing];
-  int32_t ent[kGRing];            // (head << 16) | seg slot
 };
 
 // Lane-parallel metadata of a 32-entry window: lane l describes entry base+l.
-template <typename W, typename G>
 struct Window {
   int64_t base;
   uint64_t key;
@@ -298,9 +289,9 @@ struct Window {
   int32_t vec;      // 16-byte vector path usable for this entry's table
 };
 
-template <typename W, typename G, typename Key>
+template <typename W, typename G, typename Key, int OPT>
 __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, uint64_t prev_key, int lane,
-                                            Window<W, G>& w) {
+                                            Window& w) {
   constexpr int kVec = 16 / sizeof(W);
   const unsigned full = 0xffffffffu;
   const Key* keys = reinterpret_cast<const Key*>(p.keys);
@@ -329,14 +320,16 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
             (reinterpret_cast<uintptr_t>(grad) % min(16, (int)(sizeof(G) * kVec))) == 0;
     w.gptr = reinterpret_cast<uint64_t>(grad + ((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + doff);
     w.wptr = reinterpret_cast<uint64_t>(wbase + row * D);
-    float* mb = p.moments ? reinterpret_cast<float*>(p.moments[t]) : nullptr;
-    w.mptr = reinterpret_cast<uint64_t>(p.optim == NEO_OPT_ROWWISE_ADAGRAD ? mb + row
-                                        : p.optim == NEO_OPT_ADAGRAD    ? mb + row * D
-                                                                        : nullptr);
+    if (OPT != NEO_OPT_SGD) {
+      float* mb = reinterpret_cast<float*>(p.moments[t]);
+      w.mptr = reinterpret_cast<uint64_t>(OPT == NEO_OPT_ROWWISE_ADAGRAD ? mb + row : mb + row * D);
+    }
   }
 }
 
-template <typename W, typename G, typename Key>
+constexpr int kChunk = 128;  // sorted entries owned per warp task (4 windows)
+
+template <typename W, typename G, typename Key, int OPT>
 __global__ void __launch_bounds__(kStreamWarps * kWarp)
 tbe_stream_update_kernel(SegParams p) {
   using SM = StreamSmem<W, G>;
@@ -348,62 +341,67 @@ tbe_stream_update_kernel(SegParams p) {
   SM& sm = reinterpret_cast<SM*>(smem_raw)[warp];
   const Key* keys = reinterpret_cast<const Key*>(p.keys);
   const int64_t N = p.N;
-  const int64_t nchunks = (N + kWarp - 1) / kWarp;
+  const int64_t nchunks = (N + kChunk - 1) / kChunk;
   const int64_t nwarps = (int64_t)gridDim.x * kStreamWarps;
   const float lr = (float)p.lr, eps = (float)p.eps;
-  const int optim = p.optim;
 
   for (int64_t chunk = (int64_t)blockIdx.x * kStreamWarps + warp; chunk < nchunks; chunk += nwarps) {
-    const int64_t c0 = chunk * kWarp;
-    Window<W, G> pw;  // producer window: the chunk, then (for the last segment) its continuation
-    load_window<W, G, Key>(p, c0, c0 > 0 ? (uint64_t)keys[c0 - 1] : ~0ull, lane, pw);
-    if (pw.heads == 0) continue;  // chunk lies inside a segment started earlier
-    const int e0 = __ffs(pw.heads) - 1;
-    if (!((pw.live >> e0) & 1u)) continue;  // only invalid ids (they sort last)
-    // producer cursor (offset from c0): runs kLead entries ahead of the consumer
+    const int64_t c0 = chunk * kChunk;
+    // first segment start at or after c0 (scan the chunk's windows)
+    Window pw;
+    uint64_t prev = c0 > 0 ? (uint64_t)keys[c0 - 1] : ~0ull;
+    int e0 = -1;
+    for (int k = 0; k < kChunk / kWarp; ++k) {
+      if (c0 + k * kWarp >= N) break;
+      load_window<W, G, Key, OPT>(p, c0 + k * kWarp, prev, lane, pw);
+      if (pw.heads) {
+        e0 = k * kWarp + __ffs(pw.heads) - 1;
+        break;
+      }
+      prev = __shfl_sync(full, pw.key, kWarp - 1);
+    }
+    if (e0 < 0 || !((pw.live >> (e0 & (kWarp - 1))) & 1u)) continue;
+    Window cw = pw;  // the consumer's window (the producer's, or the one before it)
+    // producer: runs kLead entries ahead, issuing one cp.async group per entry
     int pe = e0;
-    int pend = -1;  // range end once known: first head at/after c0+32, first invalid entry, or N
-    int wslot = -1;
+    int pend = -1;  // range end once known: first head at/after c0+kChunk, first invalid entry, or N
+    int pslot = -1;
     int pD = 0, pvec = 0;
 
     auto produce = [&]() {
       if (pend < 0) {
         int l = pe - (int)(pw.base - c0);
-        if (l == kWarp) {  // slide into the next window (continuation of the last segment)
+        if (l == kWarp) {  // slide to the next window
           const uint64_t last = __shfl_sync(full, pw.key, kWarp - 1);
-          load_window<W, G, Key>(p, pw.base + kWarp, last, lane, pw);
+          load_window<W, G, Key, OPT>(p, pw.base + kWarp, last, lane, pw);
           l = 0;
         }
         const bool head = (pw.heads >> l) & 1u;
-        const bool live = (pw.live >> l) & 1u;
-        if (!live || (head && pe >= kWarp)) {
+        if (!((pw.live >> l) & 1u) || (head && pe >= kChunk)) {
           pend = pe;
         } else {
-          const uint64_t gp = __shfl_sync(full, pw.gptr, l);
-          if (head) {  // new segment: stage its weight row + moment
-            wslot = wslot + 1 == kWRing ? 0 : wslot + 1;
-            const uint64_t wp = __shfl_sync(full, pw.wptr, l);
-            const uint64_t mp = __shfl_sync(full, pw.mptr, l);
+          if (head) {  // new segment: stage its weight row (+ row-wise moment)
+            pslot = pslot + 1 == kWRing ? 0 : pslot + 1;
             pD = __shfl_sync(full, pw.D, l);
             pvec = __shfl_sync(full, pw.vec, l);
-            const W* wrow = reinterpret_cast<const W*>(wp);
+            const W* wrow = reinterpret_cast<const W*>(__shfl_sync(full, pw.wptr, l));
             if (pvec) {
-              if (lane * kVec < pD) cp_async(&sm.w[wslot][lane][0], wrow + lane * kVec, 16);
-            } else {  // unaligned table: synchronous strided staging
-              W* ws = reinterpret_cast<W*>(&sm.w[wslot][lane][0]);
+              if (lane * kVec < pD) cp_async(&sm.w[pslot][lane][0], wrow + lane * kVec, 16);
+            } else {  // unaligned table: synchronous strided staging (own lane's slice)
+              W* ws = reinterpret_cast<W*>(&sm.w[pslot][lane][0]);
 #pragma unroll
               for (int e = 0; e < kVec; ++e) {
                 const int j = lane + e * kWarp;
                 ws[e] = j < pD ? wrow[j] : W(0);
               }
             }
-            if (lane == 0) {
-              if (optim == NEO_OPT_ROWWISE_ADAGRAD) cp_async(&sm.mr[wslot], reinterpret_cast<const float*>(mp), 4);
-              sm.seg[wslot] = SegMeta{wp, mp, pD, pvec};
+            if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
+              const uint64_t mp = __shfl_sync(full, pw.mptr, l);
+              if (lane == 0) cp_async(&sm.mr[pslot], reinterpret_cast<const float*>(mp), 4);
             }
           }
           const int gs = pe & (kGRing - 1);
-          const G* grow = reinterpret_cast<const G*>(gp);
+          const G* grow = reinterpret_cast<const G*>(__shfl_sync(full, pw.gptr, l));
           if (pvec) {
             if (lane * kVec < pD) {
               if constexpr (kGB == 32) {
@@ -421,64 +419,64 @@ tbe_stream_update_kernel(SegParams p) {
               gsm[e] = j < pD ? grow[j] : G(0);
             }
           }
-          if (lane == 0) sm.ent[gs] = ((head ? 1 : 0) << 16) | wslot;
           ++pe;
         }
       }
       cp_commit();
     };
 
+    // consumer state: current segment (registers) and its accumulator
     float acc[kVec];
 #pragma unroll
     for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
-    int cur = -1;
+    int cslot = -1;
+    uint64_t cw_w = 0, cw_m = 0;
+    int cD = 0, cvec = 0;
+    bool lane_live = false;
 
-    auto finalize = [&](int slot) {  // one optimizer step (embedding.py:212-254)
-      const SegMeta sg = sm.seg[slot];
-      bool nz = false;
-      float ss = 0.f;
+    auto finalize = [&]() {  // exactly one optimizer step for the row (embedding.py:212-254)
+      if (!lane_live) {
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) {
-        nz |= acc[e] != 0.f;
-        ss += acc[e] * acc[e];
+        for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
       }
-      if (optim == NEO_OPT_SGD || __any_sync(full, nz)) {
-        float denom = 1.f;
-        if (optim == NEO_OPT_ROWWISE_ADAGRAD) {
+      bool nz = false;
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) nz |= acc[e] != 0.f;
+      if (OPT == NEO_OPT_SGD || __any_sync(full, nz)) {
+        const W* wsm = reinterpret_cast<const W*>(&sm.w[cslot][lane][0]);
+        float scale = lr;
+        if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
+          float ss = 0.f;
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) ss += acc[e] * acc[e];
           ss = warp_sum(ss);
-          const float m = __shfl_sync(full, sm.mr[slot], 0) + ss / (float)sg.D;
-          if (lane == 0) *reinterpret_cast<float*>(sg.m) = m;
-          denom = sqrtf(m) + eps;
+          const float m = __shfl_sync(full, sm.mr[cslot], 0) + ss / (float)cD;
+          if (lane == 0) *reinterpret_cast<float*>(cw_m) = m;
+          scale = lr / (sqrtf(m) + eps);
         }
-        const float step_scale = lr / denom;
-        const W* wsm = reinterpret_cast<const W*>(&sm.w[slot][lane][0]);
         W out[kVec];
         float mo[kVec];
 #pragma unroll
         for (int e = 0; e < kVec; ++e) {
           const float w = Elem<W>::to_f(wsm[e]);
-          float r;
-          if (optim == NEO_OPT_ADAGRAD) {  // element-wise state read here (not staged)
-            const int j = sg.vec ? lane * kVec + e : lane + e * kWarp;
-            const float mj = (j < sg.D ? reinterpret_cast<const float*>(sg.m)[j] : 0.f) + acc[e] * acc[e];
+          if (OPT == NEO_OPT_ADAGRAD) {  // element-wise state read here (not staged)
+            const int j = cvec ? lane * kVec + e : lane + e * kWarp;
+            const float mj = (j < cD ? reinterpret_cast<const float*>(cw_m)[j] : 0.f) + acc[e] * acc[e];
             mo[e] = mj;
-            r = w - lr * acc[e] / (sqrtf(mj) + eps);
-          } else if (optim == NEO_OPT_ROWWISE_ADAGRAD) {
-            r = w - acc[e] * step_scale;
+            out[e] = Elem<W>::from_f(w - lr * acc[e] / (sqrtf(mj) + eps));
           } else {
-            r = w - lr * acc[e];
+            out[e] = Elem<W>::from_f(w - acc[e] * scale);
           }
-          out[e] = Elem<W>::from_f(r);
         }
-        W* wrow = reinterpret_cast<W*>(sg.w);
-        float* mrow = reinterpret_cast<float*>(sg.m);
-        if (sg.vec) {
-          if (lane * kVec < sg.D) {
+        W* wrow = reinterpret_cast<W*>(cw_w);
+        float* mrow = reinterpret_cast<float*>(cw_m);
+        if (cvec) {
+          if (lane_live) {
             Vec<W, kVec> o;
 #pragma unroll
             for (int e = 0; e < kVec; ++e) o.v[e] = out[e];
             st_vec<W, kVec>(wrow + lane * kVec, o);
-            if (optim == NEO_OPT_ADAGRAD) {
+            if (OPT == NEO_OPT_ADAGRAD) {
 #pragma unroll
               for (int e = 0; e < kVec; ++e) mrow[lane * kVec + e] = mo[e];
             }
@@ -487,9 +485,9 @@ tbe_stream_update_kernel(SegParams p) {
 #pragma unroll
           for (int e = 0; e < kVec; ++e) {
             const int j = lane + e * kWarp;
-            if (j < sg.D) {
+            if (j < cD) {
               wrow[j] = out[e];
-              if (optim == NEO_OPT_ADAGRAD) mrow[j] = mo[e];
+              if (OPT == NEO_OPT_ADAGRAD) mrow[j] = mo[e];
             }
           }
         }
@@ -504,27 +502,33 @@ tbe_stream_update_kernel(SegParams p) {
     for (int ce = e0;; ++ce) {
       produce();
       if (pend >= 0 && ce >= pend) break;
-      cp_wait<kLead>();
-      __syncwarp();
-      const int gs = ce & (kGRing - 1);
-      const int ent = sm.ent[gs];
-      if (ent >> 16) {
-        if (cur >= 0) finalize(cur);
-        cur = ent & 0xffff;
+      int l = ce - (int)(cw.base - c0);
+      if (l == kWarp) {  // the producer is already in the next window
+        cw = pw;
+        l = 0;
       }
-      const G* gsm = reinterpret_cast<const G*>(&sm.g[gs][lane][0]);
+      cp_wait<kLead>();
+      if ((cw.heads >> l) & 1u) {
+        if (cslot >= 0) finalize();
+        cslot = cslot + 1 == kWRing ? 0 : cslot + 1;
+        cw_w = __shfl_sync(full, cw.wptr, l);
+        if (OPT != NEO_OPT_SGD) cw_m = __shfl_sync(full, cw.mptr, l);
+        cD = __shfl_sync(full, cw.D, l);
+        cvec = __shfl_sync(full, cw.vec, l);
+        lane_live = cvec ? lane * kVec < cD : true;
+      }
+      const G* gsm = reinterpret_cast<const G*>(&sm.g[ce & (kGRing - 1)][lane][0]);
 #pragma unroll
       for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
     }
-    if (cur >= 0) finalize(cur);
+    if (cslot >= 0) finalize();
     cp_wait<0>();
-    __syncwarp();
   }
 }
 
-template <typename W, typename G, typename Key>
-static int launch_stream(const SegParams& p, cudaStream_t s) {
-  auto kern = tbe_stream_update_kernel<W, G, Key>;
+template <typename W, typename G, typename Key, int OPT>
+static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
+  auto kern = tbe_stream_update_kernel<W, G, Key, OPT>;
   const size_t smem = sizeof(StreamSmem<W, G>) * kStreamWarps;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -534,13 +538,22 @@ static int launch_stream(const SegParams& p, cudaStream_t s) {
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kStreamWarps * kWarp, smem);
   if (per_sm < 1) per_sm = 1;
-  const int64_t chunks = (p.N + kWarp - 1) / kWarp;
+  const int64_t chunks = (p.N + kChunk - 1) / kChunk;
   const int64_t max_blocks = (chunks + kStreamWarps - 1) / kStreamWarps;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > max_blocks) grid = max_blocks;
   if (grid < 1) grid = 1;
   kern<<<(unsigned)grid, kStreamWarps * kWarp, smem, s>>>(p);
   return check_launch("neo_tbe_backward(stream)");
+}
+
+template <typename W, typename G, typename Key>
+static int launch_stream(const SegParams& p, cudaStream_t s) {
+  switch (p.optim) {
+    case NEO_OPT_SGD: return launch_stream_opt<W, G, Key, NEO_OPT_SGD>(p, s);
+    case NEO_OPT_ROWWISE_ADAGRAD: return launch_stream_opt<W, G, Key, NEO_OPT_ROWWISE_ADAGRAD>(p, s);
+    default: return launch_stream_opt<W, G, Key, NEO_OPT_ADAGRAD>(p, s);
+  }
 }
 
 template <typename Key>
