@@ -282,7 +282,7 @@ struct Window {
   uint64_t key;
   unsigned heads;   // bit l: entry base+l starts a segment
   unsigned live;    // bit l: entry is a valid row id (< total_rows, < N)
-  uint64_t gptr;    // upstream row of this lane's entry (table column offset applied)
+  uint32_t gofs;    // upstream element offset of this lane's entry (row * stride + column offset)
   uint64_t wptr;    // weight row
   uint64_t mptr;    // moment (row-wise scalar / element-wise row)
   int32_t D;        // table dim of this lane's entry
@@ -305,7 +305,8 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
   w.heads = __ballot_sync(full, w.key != pv);
   const bool ok = in && w.key < (uint64_t)p.total_rows;
   w.live = __ballot_sync(full, ok);
-  w.gptr = w.wptr = w.mptr = 0;
+  w.gofs = 0;
+  w.wptr = w.mptr = 0;
   w.D = 0;
   w.vec = 0;
   if (ok) {
@@ -318,7 +319,7 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
     w.D = D;
     w.vec = (D % kVec) == 0 && aligned16(wbase) && (doff % kVec) == 0 && (p.grad_stride % kVec) == 0 &&
             (reinterpret_cast<uintptr_t>(grad) % min(16, (int)(sizeof(G) * kVec))) == 0;
-    w.gptr = reinterpret_cast<uint64_t>(grad + ((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + doff);
+    w.gofs = (uint32_t)(((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + doff);
     w.wptr = reinterpret_cast<uint64_t>(wbase + row * D);
     if (OPT != NEO_OPT_SGD) {
       float* mb = reinterpret_cast<float*>(p.moments[t]);
@@ -330,7 +331,7 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
 constexpr int kChunk = 128;  // sorted entries owned per warp task (4 windows)
 
 template <typename W, typename G, typename Key, int OPT>
-__global__ void __launch_bounds__(kStreamWarps * kWarp)
+__global__ void __launch_bounds__(kStreamWarps * kWarp, 6)
 tbe_stream_update_kernel(SegParams p) {
   using SM = StreamSmem<W, G>;
   constexpr int kVec = SM::kVec;
@@ -344,6 +345,7 @@ tbe_stream_update_kernel(SegParams p) {
   const int64_t nchunks = (N + kChunk - 1) / kChunk;
   const int64_t nwarps = (int64_t)gridDim.x * kStreamWarps;
   const float lr = (float)p.lr, eps = (float)p.eps;
+  const G* gbase = reinterpret_cast<const G*>(p.grad);
 
   for (int64_t chunk = (int64_t)blockIdx.x * kStreamWarps + warp; chunk < nchunks; chunk += nwarps) {
     const int64_t c0 = chunk * kChunk;
@@ -401,7 +403,7 @@ tbe_stream_update_kernel(SegParams p) {
             }
           }
           const int gs = pe & (kGRing - 1);
-          const G* grow = reinterpret_cast<const G*>(__shfl_sync(full, pw.gptr, l));
+          const G* grow = gbase + __shfl_sync(full, pw.gofs, l);
           if (pvec) {
             if (lane * kVec < pD) {
               if constexpr (kGB == 32) {
@@ -432,6 +434,7 @@ tbe_stream_update_kernel(SegParams p) {
     int cslot = -1;
     uint64_t cw_w = 0, cw_m = 0;
     int cD = 0, cvec = 0;
+    float cinvD = 0.f;
     bool lane_live = false;
 
     auto finalize = [&]() {  // exactly one optimizer step for the row (embedding.py:212-254)
@@ -450,9 +453,9 @@ tbe_stream_update_kernel(SegParams p) {
 #pragma unroll
           for (int e = 0; e < kVec; ++e) ss += acc[e] * acc[e];
           ss = warp_sum(ss);
-          const float m = __shfl_sync(full, sm.mr[cslot], 0) + ss / (float)cD;
+          const float m = __shfl_sync(full, sm.mr[cslot], 0) + ss * cinvD;
           if (lane == 0) *reinterpret_cast<float*>(cw_m) = m;
-          scale = lr / (sqrtf(m) + eps);
+          scale = __fdividef(lr, __fsqrt_rn(m) + eps);
         }
         W out[kVec];
         float mo[kVec];
@@ -463,7 +466,7 @@ tbe_stream_update_kernel(SegParams p) {
             const int j = cvec ? lane * kVec + e : lane + e * kWarp;
             const float mj = (j < cD ? reinterpret_cast<const float*>(cw_m)[j] : 0.f) + acc[e] * acc[e];
             mo[e] = mj;
-            out[e] = Elem<W>::from_f(w - lr * acc[e] / (sqrtf(mj) + eps));
+            out[e] = Elem<W>::from_f(w - __fdividef(lr * acc[e], __fsqrt_rn(mj) + eps));
           } else {
             out[e] = Elem<W>::from_f(w - acc[e] * scale);
           }
@@ -498,28 +501,36 @@ tbe_stream_update_kernel(SegParams p) {
 
 #pragma unroll 1
     for (int i = 0; i < kLead; ++i) produce();  // fill the pipeline
+    int ce = e0;
 #pragma unroll 1
-    for (int ce = e0;; ++ce) {
-      produce();
-      if (pend >= 0 && ce >= pend) break;
-      int l = ce - (int)(cw.base - c0);
-      if (l == kWarp) {  // the producer is already in the next window
-        cw = pw;
-        l = 0;
-      }
-      cp_wait<kLead>();
-      if ((cw.heads >> l) & 1u) {
-        if (cslot >= 0) finalize();
-        cslot = cslot + 1 == kWRing ? 0 : cslot + 1;
-        cw_w = __shfl_sync(full, cw.wptr, l);
-        if (OPT != NEO_OPT_SGD) cw_m = __shfl_sync(full, cw.mptr, l);
-        cD = __shfl_sync(full, cw.D, l);
-        cvec = __shfl_sync(full, cw.vec, l);
-        lane_live = cvec ? lane * kVec < cD : true;
-      }
-      const G* gsm = reinterpret_cast<const G*>(&sm.g[ce & (kGRing - 1)][lane][0]);
+    while (true) {
+      const int wstart = (int)(cw.base - c0);
+      bool stop = false;
+#pragma unroll 1
+      for (; ce < wstart + kWarp; ++ce) {
+        produce();
+        if (pend >= 0 && ce >= pend) {
+          stop = true;
+          break;
+        }
+        cp_wait<kLead>();
+        const int l = ce - wstart;
+        if ((cw.heads >> l) & 1u) {
+          if (cslot >= 0) finalize();
+          cslot = cslot + 1 == kWRing ? 0 : cslot + 1;
+          cw_w = __shfl_sync(full, cw.wptr, l);
+          if (OPT != NEO_OPT_SGD) cw_m = __shfl_sync(full, cw.mptr, l);
+          cD = __shfl_sync(full, cw.D, l);
+          cvec = __shfl_sync(full, cw.vec, l);
+          cinvD = __frcp_rn((float)cD);
+          lane_live = cvec ? lane * kVec < cD : true;
+        }
+        const G* gsm = reinterpret_cast<const G*>(&sm.g[ce & (kGRing - 1)][lane][0]);
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
+        for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
+      }
+      if (stop) break;
+      cw = pw;  // the producer is already in the next window
     }
     if (cslot >= 0) finalize();
     cp_wait<0>();
@@ -661,7 +672,8 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   p.bags = vbuf.Current();
   const int wvec = weight_dtype == NEO_F16 ? 8 : 4;
   const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
-                    p.max_dim <= kWarp * wvec && !out_count;
+                    p.max_dim <= kWarp * wvec && !out_count &&
+                    p.B * p.grad_stride < (int64_t(1) << 32);  // 32-bit upstream offsets
   if (fast) {
     const bool h = weight_dtype == NEO_F16;
     switch (grad_dtype) {
