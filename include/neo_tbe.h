@@ -69,6 +69,11 @@ enum {
   NEO_BWD_AGGREGATE = 1, /* emit RowGradients (ids ascending, grads) only */
   NEO_BWD_DENSE = 2      /* write aggregated rows into dense per-table gradients */
 };
+/* optional layout promises OR-ed into `mode` (UPDATE fast path):
+ * ALIGNED: every table's D is a multiple of the 16-byte vector, weight rows
+ *          and the gradient (base, stride, column offsets) are 16-byte aligned;
+ * FULL_ROWS: additionally every D equals 32 vectors (128 f32 / 256 f16). */
+enum { NEO_BWD_FLAG_ALIGNED = 0x100, NEO_BWD_FLAG_FULL_ROWS = 0x200 };
 
 /* Device-side error record (caller allocates sizeof(neo_error) bytes of
  * device memory).  position = first offending position in index-buffer

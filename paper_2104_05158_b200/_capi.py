@@ -20,6 +20,7 @@ NEO_I32, NEO_I64 = 0, 1
 NEO_POOL_SUM, NEO_POOL_MEAN = 0, 1
 NEO_OPT_SGD, NEO_OPT_ROWWISE_ADAGRAD, NEO_OPT_ADAGRAD, NEO_OPT_NONE = 0, 1, 2, 3
 NEO_BWD_UPDATE, NEO_BWD_AGGREGATE, NEO_BWD_DENSE = 0, 1, 2
+NEO_BWD_FLAG_ALIGNED, NEO_BWD_FLAG_FULL_ROWS = 0x100, 0x200
 
 P = C.c_void_p
 I32 = C.c_int32

@@ -115,6 +115,7 @@ struct SegParams {
   const int32_t* seg_starts;
   const int64_t* num_segs;
   int64_t N;
+  int32_t flags;   // NEO_BWD_FLAG_* layout promises from the caller
 };
 
 // aggregate the segment's upstream rows into g (warp-private smem row)
@@ -262,6 +263,33 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem, int bytes
   else
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
 }
+// L2 residency control: the upstream slice of the table being updated is
+// re-read ~L times (once per occurrence) and must stay in L2, while weight
+// rows, moments and the sorted (key, bag) stream are touched once.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void cp_async_hint(void* smem, const void* gmem, int bytes, uint64_t pol) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  if (bytes == 16)
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "l"(pol));
+  else if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "l"(pol));
+  else
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gmem), "l"(pol));
+}
+__device__ __forceinline__ void st_v4_hint(void* gmem, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(gmem), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
@@ -298,8 +326,8 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
   const int64_t j = base + lane;
   w.base = base;
   const bool in = j < p.N;
-  w.key = in ? (uint64_t)keys[j] : ~0ull;
-  const int32_t bag = in ? p.bags[j] : 0;
+  w.key = in ? (uint64_t)__ldcs(keys + j) : ~0ull;
+  const int32_t bag = in ? __ldcs(p.bags + j) : 0;
   uint64_t pv = __shfl_up_sync(full, w.key, 1);
   if (lane == 0) pv = prev_key;
   w.heads = __ballot_sync(full, w.key != pv);
@@ -330,7 +358,7 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
 
 constexpr int kChunk = 128;  // sorted entries owned per warp task (4 windows)
 
-template <typename W, typename G, typename Key, int OPT>
+template <typename W, typename G, typename Key, int OPT, bool FULL>
 __global__ void __launch_bounds__(kStreamWarps * kWarp, 6)
 tbe_stream_update_kernel(SegParams p) {
   using SM = StreamSmem<W, G>;
@@ -346,6 +374,8 @@ tbe_stream_update_kernel(SegParams p) {
   const int64_t nwarps = (int64_t)gridDim.x * kStreamWarps;
   const float lr = (float)p.lr, eps = (float)p.eps;
   const G* gbase = reinterpret_cast<const G*>(p.grad);
+  const uint64_t pol_stream = l2_evict_first();
+  const uint64_t pol_keep = l2_evict_last();
 
   for (int64_t chunk = (int64_t)blockIdx.x * kStreamWarps + warp; chunk < nchunks; chunk += nwarps) {
     const int64_t c0 = chunk * kChunk;
@@ -384,11 +414,13 @@ tbe_stream_update_kernel(SegParams p) {
         } else {
           if (head) {  // new segment: stage its weight row (+ row-wise moment)
             pslot = pslot + 1 == kWRing ? 0 : pslot + 1;
-            pD = __shfl_sync(full, pw.D, l);
-            pvec = __shfl_sync(full, pw.vec, l);
+            if (!FULL) {
+              pD = __shfl_sync(full, pw.D, l);
+              pvec = __shfl_sync(full, pw.vec, l);
+            }
             const W* wrow = reinterpret_cast<const W*>(__shfl_sync(full, pw.wptr, l));
-            if (pvec) {
-              if (lane * kVec < pD) cp_async(&sm.w[pslot][lane][0], wrow + lane * kVec, 16);
+            if (FULL || pvec) {
+              if (FULL || lane * kVec < pD) cp_async_hint(&sm.w[pslot][lane][0], wrow + lane * kVec, 16, pol_stream);
             } else {  // unaligned table: synchronous strided staging (own lane's slice)
               W* ws = reinterpret_cast<W*>(&sm.w[pslot][lane][0]);
 #pragma unroll
@@ -399,18 +431,18 @@ tbe_stream_update_kernel(SegParams p) {
             }
             if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
               const uint64_t mp = __shfl_sync(full, pw.mptr, l);
-              if (lane == 0) cp_async(&sm.mr[pslot], reinterpret_cast<const float*>(mp), 4);
+              if (lane == 0) cp_async_hint(&sm.mr[pslot], reinterpret_cast<const float*>(mp), 4, pol_stream);
             }
           }
           const int gs = pe & (kGRing - 1);
           const G* grow = gbase + __shfl_sync(full, pw.gofs, l);
-          if (pvec) {
-            if (lane * kVec < pD) {
+          if (FULL || pvec) {
+            if (FULL || lane * kVec < pD) {
               if constexpr (kGB == 32) {
-                cp_async(&sm.g[gs][lane][0], grow + lane * kVec, 16);
-                cp_async(&sm.g[gs][lane][16], grow + lane * kVec + kVec / 2, 16);
+                cp_async_hint(&sm.g[gs][lane][0], grow + lane * kVec, 16, pol_keep);
+                cp_async_hint(&sm.g[gs][lane][16], grow + lane * kVec + kVec / 2, 16, pol_keep);
               } else {
-                cp_async(&sm.g[gs][lane][0], grow + lane * kVec, kGB);
+                cp_async_hint(&sm.g[gs][lane][0], grow + lane * kVec, kGB, pol_keep);
               }
             }
           } else {
@@ -438,7 +470,7 @@ tbe_stream_update_kernel(SegParams p) {
     bool lane_live = false;
 
     auto finalize = [&]() {  // exactly one optimizer step for the row (embedding.py:212-254)
-      if (!lane_live) {
+      if (!FULL && !lane_live) {
 #pragma unroll
         for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
       }
@@ -473,12 +505,12 @@ tbe_stream_update_kernel(SegParams p) {
         }
         W* wrow = reinterpret_cast<W*>(cw_w);
         float* mrow = reinterpret_cast<float*>(cw_m);
-        if (cvec) {
-          if (lane_live) {
+        if (FULL || cvec) {
+          if (FULL || lane_live) {
             Vec<W, kVec> o;
 #pragma unroll
             for (int e = 0; e < kVec; ++e) o.v[e] = out[e];
-            st_vec<W, kVec>(wrow + lane * kVec, o);
+            st_v4_hint(wrow + lane * kVec, *reinterpret_cast<const uint4*>(&o), pol_stream);
             if (OPT == NEO_OPT_ADAGRAD) {
 #pragma unroll
               for (int e = 0; e < kVec; ++e) mrow[lane * kVec + e] = mo[e];
@@ -520,10 +552,17 @@ tbe_stream_update_kernel(SegParams p) {
           cslot = cslot + 1 == kWRing ? 0 : cslot + 1;
           cw_w = __shfl_sync(full, cw.wptr, l);
           if (OPT != NEO_OPT_SGD) cw_m = __shfl_sync(full, cw.mptr, l);
-          cD = __shfl_sync(full, cw.D, l);
-          cvec = __shfl_sync(full, cw.vec, l);
-          cinvD = __frcp_rn((float)cD);
-          lane_live = cvec ? lane * kVec < cD : true;
+          if (FULL) {
+            cD = kWarp * kVec;
+            cvec = 1;
+            cinvD = 1.0f / (float)(kWarp * kVec);
+            lane_live = true;
+          } else {
+            cD = __shfl_sync(full, cw.D, l);
+            cvec = __shfl_sync(full, cw.vec, l);
+            cinvD = __frcp_rn((float)cD);
+            lane_live = cvec ? lane * kVec < cD : true;
+          }
         }
         const G* gsm = reinterpret_cast<const G*>(&sm.g[ce & (kGRing - 1)][lane][0]);
 #pragma unroll
@@ -539,7 +578,9 @@ tbe_stream_update_kernel(SegParams p) {
 
 template <typename W, typename G, typename Key, int OPT>
 static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
-  auto kern = tbe_stream_update_kernel<W, G, Key, OPT>;
+  const bool full_rows = (p.flags & NEO_BWD_FLAG_FULL_ROWS) != 0;
+  auto kern = full_rows ? tbe_stream_update_kernel<W, G, Key, OPT, true>
+                        : tbe_stream_update_kernel<W, G, Key, OPT, false>;
   const size_t smem = sizeof(StreamSmem<W, G>) * kStreamWarps;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -763,18 +804,19 @@ extern "C" int neo_tbe_backward(int32_t num_tables, int64_t batch, const int64_t
     return fail(NEO_E_ARG, "neo_tbe_backward: negative size");
   if ((int64_t)num_tables * batch >= INT_MAX || num_indices >= INT_MAX)
     return fail(NEO_E_ARG, "neo_tbe_backward: more than 2^31 bags or indices in one call");
-  if (mode != NEO_BWD_UPDATE && mode != NEO_BWD_AGGREGATE && mode != NEO_BWD_DENSE)
+  const int32_t base_mode = mode & 0xff;
+  if (base_mode != NEO_BWD_UPDATE && base_mode != NEO_BWD_AGGREGATE && base_mode != NEO_BWD_DENSE)
     return fail(NEO_E_ARG, "neo_tbe_backward: bad mode");
-  if (mode == NEO_BWD_UPDATE) {
+  if (base_mode == NEO_BWD_UPDATE) {
     if (optim != NEO_OPT_SGD && optim != NEO_OPT_ROWWISE_ADAGRAD && optim != NEO_OPT_ADAGRAD)
       return fail(NEO_E_ARG, "cfg.kind: unknown optimizer");
     if (!(lr > 0)) return fail(NEO_E_ARG, "lr: must be > 0");
     if (eps < 0) return fail(NEO_E_ARG, "eps: must be >= 0");
     if (optim != NEO_OPT_SGD && !moments) return fail(NEO_E_ARG, "moment: state required");
   }
-  if (mode == NEO_BWD_AGGREGATE && (!out_ids || !out_grads))
+  if (base_mode == NEO_BWD_AGGREGATE && (!out_ids || !out_grads))
     return fail(NEO_E_ARG, "neo_tbe_backward: AGGREGATE needs out_ids/out_grads");
-  if (mode == NEO_BWD_DENSE && !dense_grads)
+  if (base_mode == NEO_BWD_DENSE && !dense_grads)
     return fail(NEO_E_ARG, "neo_tbe_backward: DENSE needs dense_grads");
   if (pooling != NEO_POOL_SUM && pooling != NEO_POOL_MEAN)
     return fail(NEO_E_ARG, "neo_tbe_backward: pooling must be SUM or MEAN");
@@ -798,7 +840,8 @@ extern "C" int neo_tbe_backward(int32_t num_tables, int64_t batch, const int64_t
   p.grad_stride = grad_stride;
   p.pooling = pooling;
   p.offsets = offsets;
-  p.mode = mode;
+  p.mode = mode & 0xff;
+  p.flags = mode & ~0xff;
   p.optim = optim;
   p.lr = lr;
   p.eps = eps;

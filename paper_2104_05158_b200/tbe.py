@@ -189,6 +189,15 @@ class TableGroup:
             dense_ptrs = _u64_ptrs(dense_grads, self.device)
         optim = optim or self.optim or "sgd"
         stride = grad.stride(0) if grad.dim() == 2 else self.total_dim
+        if mode == "update":  # layout promises that select the specialised fast path
+            vec = 16 // torch.empty(0, dtype=self.dtype).element_size()
+            aligned = (all(d % vec == 0 for d in self.dims) and stride % vec == 0
+                       and grad.data_ptr() % 16 == 0
+                       and all(w is None or w.data_ptr() % 16 == 0 for w in self.weights))
+            if aligned:
+                mode_code |= capi.NEO_BWD_FLAG_ALIGNED
+                if all(d == 32 * vec for d in self.dims):
+                    mode_code |= capi.NEO_BWD_FLAG_FULL_ROWS
         rc = capi.lib().neo_tbe_backward(
             self.T, batch, self.row_offsets.data_ptr(), self.total_rows, self.dim_offsets.data_ptr(),
             self.max_dim, self.weight_ptrs.data_ptr(), DTYPE_CODE[self.dtype],
