@@ -196,8 +196,11 @@ def test_group_forward_f32_tolerance(pkg, wdtype, idtype):
 
 # dims sets: the first has a 256-wide f32 table (general segment kernel), the
 # second fits the streamed fast path (incl. an unaligned D=100 table)
+# (f32 D=128 / f16 D=256 tables select the guard-free FULL_ROWS kernel)
 @pytest.mark.parametrize("dims,rows", [([64, 128, 32, 256], [3000, 5000, 800, 2000]),
-                                       ([64, 128, 32, 8, 100], [3000, 5000, 40, 2000, 700])])
+                                       ([64, 128, 32, 8, 100], [3000, 5000, 40, 2000, 700]),
+                                       ([128, 128, 128], [4000, 300, 9000]),
+                                       ([256, 256], [3000, 500])])
 @pytest.mark.parametrize("kind", ["rowwise_adagrad", "adagrad", "sgd"])
 @pytest.mark.parametrize("gdtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("wdtype", [torch.float32, torch.float16])
