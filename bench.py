@@ -284,10 +284,13 @@ def run_b200(a, rank, world):
     upstream = torch.ones((B, T * D), dtype=torch.float32, device=dev)
     U_list = [int(torch.unique(batches[0][t * N:(t + 1) * N]).numel()) for t in range(T)]
 
+    counts = [N] * T  # host-known per-table id counts (lengths are host data)
+
     def step(i):
         ix = batches[i % 2]
         grp.forward(ix, offsets, B, out=out)
-        grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS)
+        grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS,
+                     table_counts=counts)
 
     for i in range(a.warmup):
         step(i)
@@ -304,7 +307,8 @@ def run_b200(a, rank, world):
         ix = batches[i % 2]
         grp.forward(ix, offsets, B, out=out)
         e1.record()
-        grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS)
+        grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS,
+                     table_counts=counts)
         e2.record()
     torch.cuda.synchronize()
     clk = clocks.stop()

@@ -43,16 +43,21 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile every csrc/*.cu for sm_100a and link libneob200.so."""
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path = None) -> Path:
+    """Compile every csrc/*.cu for sm_100a and link libneob200.so (or `out`
+    with extra -D defines, for A/B experiments)."""
+    lib = LIB if out is None else Path(out)
+    if out is None and not defines and not force and not _stale():
         return LIB
-    OBJ.mkdir(exist_ok=True)
+    obj_dir = OBJ if out is None else OBJ / lib.stem
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    obj_dir.mkdir(parents=True, exist_ok=True)
     cc = nvcc()
 
     def compile_one(src: Path) -> Path:
-        obj = OBJ / (src.stem + ".o")
-        cmd = [cc, *ARCH, *FLAGS, "-I", str(INCLUDE), "-I", str(CSRC), "-c", str(src), "-o", str(obj)]
+        obj = obj_dir / (src.stem + ".o")
+        cmd = [cc, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", str(INCLUDE), "-I", str(CSRC), "-c",
+               str(src), "-o", str(obj)]
         if verbose:
             print(" ".join(cmd), flush=True)
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -64,13 +69,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, sources()))
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     cmd = [cc, *ARCH, "-shared", "-o", str(tmp), *map(str, objs)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

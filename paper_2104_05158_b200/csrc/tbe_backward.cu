@@ -276,6 +276,11 @@ __device__ __forceinline__ uint64_t l2_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
   return pol;
 }
+__device__ __forceinline__ uint64_t l2_evict_normal() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void cp_async_hint(void* smem, const void* gmem, int bytes, uint64_t pol) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   if (bytes == 16)
@@ -374,8 +379,12 @@ tbe_stream_update_kernel(SegParams p) {
   const int64_t nwarps = (int64_t)gridDim.x * kStreamWarps;
   const float lr = (float)p.lr, eps = (float)p.eps;
   const G* gbase = reinterpret_cast<const G*>(p.grad);
-  const uint64_t pol_stream = l2_evict_first();
-  const uint64_t pol_keep = l2_evict_last();
+#ifndef NEO_L2_HINTS
+#define NEO_L2_HINTS 2
+#endif
+  // 0: no hints; 1: evict_first weights + evict_last upstream; 2: evict_last upstream only
+  const uint64_t pol_stream = NEO_L2_HINTS == 1 ? l2_evict_first() : l2_evict_normal();
+  const uint64_t pol_keep = NEO_L2_HINTS == 0 ? l2_evict_normal() : l2_evict_last();
 
   for (int64_t chunk = (int64_t)blockIdx.x * kStreamWarps + warp; chunk < nchunks; chunk += nwarps) {
     const int64_t c0 = chunk * kChunk;

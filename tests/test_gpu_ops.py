@@ -291,3 +291,26 @@ def test_mean_pooling_and_fp16_output(pkg):
     want_mean = np.where(L > 0, s / np.maximum(L, 1), 0.0)
     assert np.allclose(m, want_mean, rtol=1e-6, atol=1e-6)
     assert np.array_equal(h, O.fp16_roundtrip(s.astype(np.float32))[0])
+
+
+def test_backward_subgroup_split_bitwise(pkg, monkeypatch):
+    """UPDATE split into sub-groups with shorter sort keys (table_counts) is
+    bit-identical to the single-call backward."""
+    from paper_2104_05158_b200 import tbe
+
+    monkeypatch.setattr(tbe, "SORT_BITS", 13)  # 8192 rows per sub-group
+    rng = np.random.default_rng(21)
+    rows, dims, B = [3000, 5000, 2000, 7000, 100], [128] * 5, 512
+    lengths, idx = _random_group_case(rng, 5, rows, dims, B, 20)
+    res = []
+    for counts in (None, lengths.sum(axis=1).tolist()):
+        torch.manual_seed(0)
+        grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim="rowwise_adagrad")
+        grp._storage.normal_()
+        off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+        ix = torch.from_numpy(idx).int().cuda()
+        g = torch.randn((B, grp.total_dim), device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+        grp.backward(ix, off, B, g, mode="update", optim="rowwise_adagrad", lr=0.05, eps=1e-8, table_counts=counts)
+        res.append((grp._storage.cpu(), torch.cat([m.cpu() for m in grp.moments])))
+    assert len(grp._sort_groups()) > 1
+    assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
