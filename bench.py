@@ -50,6 +50,10 @@ def parse_args(argv=None):
     p.add_argument("--pooling", type=int, default=32)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-subgroups", action="store_true",
+                   help="diagnostic: one backward call over all tables (no shorter sort keys)")
+    p.add_argument("--upstream-broadcast", action="store_true",
+                   help="diagnostic: one upstream row for every bag (stride 0); not a valid bench number")
     p.add_argument("--cpu-sample-batch", type=int, default=0,
                    help="samples per table in one CPU-baseline sample (default: full batch)")
     return p.parse_args(argv)
@@ -282,9 +286,11 @@ def run_b200(a, rank, world):
     batches = [torch.randint(0, H, (T * N,), dtype=torch.int32, device=dev) for _ in range(2)]
     out = torch.empty((B, T * D), dtype=torch.float32, device=dev)
     upstream = torch.ones((B, T * D), dtype=torch.float32, device=dev)
+    if a.upstream_broadcast:
+        upstream = torch.ones((1, T * D), dtype=torch.float32, device=dev).expand(B, T * D)
     U_list = [int(torch.unique(batches[0][t * N:(t + 1) * N]).numel()) for t in range(T)]
 
-    counts = [N] * T  # host-known per-table id counts (lengths are host data)
+    counts = None if a.no_subgroups else [N] * T  # host-known per-table id counts (lengths are host data)
 
     def step(i):
         ix = batches[i % 2]

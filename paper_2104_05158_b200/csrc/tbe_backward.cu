@@ -116,6 +116,7 @@ struct SegParams {
   const int64_t* num_segs;
   int64_t N;
   int32_t flags;   // NEO_BWD_FLAG_* layout promises from the caller
+  int64_t* chunk_counter;  // work-queue counter of the streamed kernel (zeroed per launch)
 };
 
 // aggregate the segment's upstream rows into g (warp-private smem row)
@@ -386,7 +387,20 @@ tbe_stream_update_kernel(SegParams p) {
   const uint64_t pol_stream = NEO_L2_HINTS == 1 ? l2_evict_first() : l2_evict_normal();
   const uint64_t pol_keep = NEO_L2_HINTS == 0 ? l2_evict_normal() : l2_evict_last();
 
-  for (int64_t chunk = (int64_t)blockIdx.x * kStreamWarps + warp; chunk < nchunks; chunk += nwarps) {
+  // Dynamic chunk scheduling: warps claim chunks from a global counter (one
+  // claim in flight ahead), so all warps stay on the same frontier of the
+  // sorted stream and the upstream slice they share stays L2-resident (a
+  // static grid stride lets warps drift apart over hundreds of chunks).
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(p.chunk_counter);
+  int64_t next = 0;
+  if (lane == 0) next = (int64_t)atomicAdd(counter, 1ull);
+  next = __shfl_sync(full, next, 0);
+  (void)nwarps;
+  for (;;) {
+    const int64_t chunk = next;
+    if (chunk >= nchunks) break;
+    if (lane == 0) next = (int64_t)atomicAdd(counter, 1ull);
+    next = __shfl_sync(full, next, 0);
     const int64_t c0 = chunk * kChunk;
     // first segment start at or after c0 (scan the chunk's windows)
     Window pw;
@@ -604,6 +618,8 @@ static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > max_blocks) grid = max_blocks;
   if (grid < 1) grid = 1;
+  if (cudaMemsetAsync(p.chunk_counter, 0, sizeof(int64_t), s) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tbe_backward: counter reset failed");
   kern<<<(unsigned)grid, kStreamWarps * kWarp, smem, s>>>(p);
   return check_launch("neo_tbe_backward(stream)");
 }
@@ -720,6 +736,7 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   const Key* keys = kbuf.Current();
   p.keys = keys;
   p.bags = vbuf.Current();
+  p.chunk_counter = nseg + 1;
   const int wvec = weight_dtype == NEO_F16 ? 8 : 4;
   const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
                     p.max_dim <= kWarp * wvec && !out_count &&
