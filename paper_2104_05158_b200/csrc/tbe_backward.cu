@@ -392,15 +392,14 @@ tbe_stream_update_kernel(SegParams p) {
   // sorted stream and the upstream slice they share stays L2-resident (a
   // static grid stride lets warps drift apart over hundreds of chunks).
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(p.chunk_counter);
-  int64_t next = 0;
-  if (lane == 0) next = (int64_t)atomicAdd(counter, 1ull);
-  next = __shfl_sync(full, next, 0);
+  __shared__ long long s_claim[kStreamWarps];
   (void)nwarps;
   for (;;) {
-    const int64_t chunk = next;
+    __syncwarp();
+    if (lane == 0) s_claim[warp] = (long long)atomicAdd(counter, 1ull);
+    __syncwarp();
+    const int64_t chunk = s_claim[warp];
     if (chunk >= nchunks) break;
-    if (lane == 0) next = (int64_t)atomicAdd(counter, 1ull);
-    next = __shfl_sync(full, next, 0);
     const int64_t c0 = chunk * kChunk;
     // first segment start at or after c0 (scan the chunk's windows)
     Window pw;
