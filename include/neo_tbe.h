@@ -128,7 +128,7 @@ int neo_tbe_forward(int32_t num_tables, int64_t batch,
  *   DENSE: dense_grads[t] (H_t x D_t, accumulator type, pre-zeroed) get the
  *         aggregated rows.
  * Workspace size: neo_tbe_backward_workspace_bytes. */
-size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows);
+size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows, int32_t max_dim);
 
 int neo_tbe_backward(int32_t num_tables, int64_t batch,
                      const int64_t* row_offsets, int64_t total_rows,

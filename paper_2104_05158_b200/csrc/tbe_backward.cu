@@ -117,6 +117,10 @@ struct SegParams {
   int64_t N;
   int32_t flags;   // NEO_BWD_FLAG_* layout promises from the caller
   int64_t* chunk_counter;  // work-queue counter of the streamed kernel (zeroed per launch)
+  int32_t* chunk_slot;     // per 128-entry chunk: partial-sum slot if the chunk lies inside one row, else -1
+  float* pool;             // partial sums of such chunks (slot x max_dim, f32)
+  unsigned* pool_counter;
+  int64_t pool_cap;
 };
 
 // aggregate the segment's upstream rows into g (warp-private smem row)
@@ -364,6 +368,80 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
 
 constexpr int kChunk = 128;  // sorted entries owned per warp task (4 windows)
 
+// Hot rows (skewed ids): a 128-entry chunk whose entries all belong to ONE
+// row (no segment boundary inside, and it does not start the row) gets its
+// upstream partial sum precomputed here, in entry order, by its own warp.
+// The streamed kernel then folds such partials into the row's gradient in
+// chunk order instead of walking the row's occurrences on a single warp, so
+// a row touched 1e5 times costs ~1e3 partial loads, not 1e5 serial gathers.
+template <typename W, typename G, typename Key>
+__global__ void __launch_bounds__(256)
+hot_chunk_kernel(SegParams p) {
+  constexpr int kVec = 16 / sizeof(W);
+  const unsigned full = 0xffffffffu;
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const Key* keys = reinterpret_cast<const Key*>(p.keys);
+  const G* grad = reinterpret_cast<const G*>(p.grad);
+  const int64_t nchunks = (p.N + kChunk - 1) / kChunk;
+  for (int64_t c = (int64_t)blockIdx.x * 8 + warp; c < nchunks; c += (int64_t)gridDim.x * 8) {
+    const int64_t c0 = c * kChunk;
+    bool bf = false;
+    if (c0 > 0 && c0 + kChunk <= p.N) {
+      const uint64_t k0 = (uint64_t)keys[c0];
+      bf = k0 < (uint64_t)p.total_rows && (uint64_t)keys[c0 - 1] == k0 && (uint64_t)keys[c0 + kChunk - 1] == k0;
+    }
+    int32_t slot = -1;
+    if (bf) {
+      unsigned sl = 0;
+      if (lane == 0) sl = atomicAdd(p.pool_counter, 1u);
+      sl = __shfl_sync(full, sl, 0);
+      slot = sl < (unsigned)p.pool_cap ? (int32_t)sl : -1;
+    }
+    if (slot >= 0) {
+      const int32_t t = p.bags[c0] / (int32_t)p.B;
+      const int32_t doff = p.dim_offsets[t];
+      const int32_t D = p.dim_offsets[t + 1] - doff;
+      const bool vec = (D % kVec) == 0 && aligned16(reinterpret_cast<const void*>(p.weights[t])) &&
+                       (doff % kVec) == 0 && (p.grad_stride % kVec) == 0 &&
+                       (reinterpret_cast<uintptr_t>(grad) % min(16, (int)(sizeof(G) * kVec))) == 0;
+      float acc[kVec];
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
+      const int32_t mybag = p.bags[c0 + lane];
+      for (int q = 0; q < kChunk; q += kWarp) {
+        const int32_t qb = p.bags[c0 + q + lane];
+#pragma unroll 8
+        for (int e2 = 0; e2 < kWarp; ++e2) {
+          const int32_t bag = __shfl_sync(full, qb, e2);
+          const G* src = grad + ((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + doff;
+          if (vec) {
+            if (lane * kVec < D) {
+              Vec<G, kVec> v = ld_vec<G, kVec>(src + lane * kVec);
+#pragma unroll
+              for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(v.v[e]);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < kVec; ++e) {
+              const int j = lane + e * kWarp;
+              if (j < D) acc[e] += Elem<G>::to_f(src[j]);
+            }
+          }
+        }
+      }
+      (void)mybag;
+      float* dst = p.pool + (int64_t)slot * p.max_dim;
+#pragma unroll
+      for (int e = 0; e < kVec; ++e) {
+        const int j = vec ? lane * kVec + e : lane + e * kWarp;
+        if (j < D) dst[j] = acc[e];
+      }
+    }
+    if (lane == 0) p.chunk_slot[c] = slot;
+  }
+}
+
+
 template <typename W, typename G, typename Key, int OPT, bool FULL>
 __global__ void __launch_bounds__(kStreamWarps * kWarp, 6)
 tbe_stream_update_kernel(SegParams p) {
@@ -419,6 +497,7 @@ tbe_stream_update_kernel(SegParams p) {
     // producer: runs kLead entries ahead, issuing one cp.async group per entry
     int pe = e0;
     int pend = -1;  // range end once known: first head at/after c0+kChunk, first invalid entry, or N
+    int64_t cont_chunk = -1;  // first hot chunk the last segment continues into
     int pslot = -1;
     int pD = 0, pvec = 0;
 
@@ -426,8 +505,16 @@ tbe_stream_update_kernel(SegParams p) {
       if (pend < 0) {
         int l = pe - (int)(pw.base - c0);
         if (l == kWarp) {  // slide to the next window
+          const int64_t nb = pw.base + kWarp;
+          if (nb % kChunk == 0 && nb < p.N && p.chunk_slot[nb / kChunk] >= 0) {
+            // the row continues through a hot chunk: its partials are folded in below
+            pend = pe;
+            cont_chunk = nb / kChunk;
+            cp_commit();
+            return;
+          }
           const uint64_t last = __shfl_sync(full, pw.key, kWarp - 1);
-          load_window<W, G, Key, OPT>(p, pw.base + kWarp, last, lane, pw);
+          load_window<W, G, Key, OPT>(p, nb, last, lane, pw);
           l = 0;
         }
         const bool head = (pw.heads >> l) & 1u;
@@ -489,6 +576,7 @@ tbe_stream_update_kernel(SegParams p) {
     uint64_t cw_w = 0, cw_m = 0;
     int cD = 0, cvec = 0;
     float cinvD = 0.f;
+    uint64_t cseg_key = 0;
     bool lane_live = false;
 
     auto finalize = [&]() {  // exactly one optimizer step for the row (embedding.py:212-254)
@@ -573,6 +661,7 @@ tbe_stream_update_kernel(SegParams p) {
           if (cslot >= 0) finalize();
           cslot = cslot + 1 == kWRing ? 0 : cslot + 1;
           cw_w = __shfl_sync(full, cw.wptr, l);
+          cseg_key = __shfl_sync(full, cw.key, l);
           if (OPT != NEO_OPT_SGD) cw_m = __shfl_sync(full, cw.mptr, l);
           if (FULL) {
             cD = kWarp * kVec;
@@ -592,6 +681,32 @@ tbe_stream_update_kernel(SegParams p) {
       }
       if (stop) break;
       cw = pw;  // the producer is already in the next window
+    }
+    if (cont_chunk >= 0 && cslot >= 0) {
+      // fold the hot chunks' partials (chunk order), then walk the row's tail
+      int64_t c = cont_chunk;
+      const int64_t nchunks_all = (N + kChunk - 1) / kChunk;
+      for (; c < nchunks_all; ++c) {
+        const int32_t slot = p.chunk_slot[c];
+        if (slot < 0) break;
+        const float* src = p.pool + (int64_t)slot * p.max_dim;
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          const int j = cvec ? lane * kVec + e : lane + e * kWarp;
+          if (j < cD) acc[e] += src[j];
+        }
+      }
+      for (int64_t e0 = c * kChunk; e0 < N; ++e0) {
+        if ((uint64_t)keys[e0] != cseg_key) break;
+        const int32_t bag = p.bags[e0];
+        const int32_t t = bag / (int32_t)p.B;
+        const G* src = gbase + ((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + p.dim_offsets[t];
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          const int j = cvec ? lane * kVec + e : lane + e * kWarp;
+          if (j < cD) acc[e] += Elem<G>::to_f(src[j]);
+        }
+      }
     }
     if (cslot >= 0) finalize();
     cp_wait<0>();
@@ -617,8 +732,15 @@ static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > max_blocks) grid = max_blocks;
   if (grid < 1) grid = 1;
-  if (cudaMemsetAsync(p.chunk_counter, 0, sizeof(int64_t), s) != cudaSuccess)
+  if (cudaMemsetAsync(p.chunk_counter, 0, 2 * sizeof(int64_t), s) != cudaSuccess)
     return fail(NEO_E_CUDA, "neo_tbe_backward: counter reset failed");
+  {
+    const int64_t hb = (chunks + 7) / 8;
+    const unsigned hgrid = (unsigned)(hb < (int64_t)sms * 16 ? (hb > 0 ? hb : 1) : (int64_t)sms * 16);
+    hot_chunk_kernel<W, G, Key><<<hgrid, 256, 0, s>>>(p);
+    const int rc = check_launch("neo_tbe_backward(hot chunks)");
+    if (rc) return rc;
+  }
   kern<<<(unsigned)grid, kStreamWarps * kWarp, smem, s>>>(p);
   return check_launch("neo_tbe_backward(stream)");
 }
@@ -655,13 +777,17 @@ static size_t cub_temp_bytes(int64_t N) {
   return sort_bytes > sel_bytes ? sort_bytes : sel_bytes;
 }
 
+static inline int64_t hot_chunks(int64_t N) { return (N + 127) / 128; }
+
 template <typename Key>
-static size_t workspace_for(int64_t N) {
+static size_t workspace_for(int64_t N, int64_t max_dim) {
   size_t b = 0;
   b += 2 * align256(sizeof(Key) * N);      // key double buffer
   b += 2 * align256(sizeof(int32_t) * N);  // bag double buffer
   b += align256(sizeof(int32_t) * N);      // segment starts
-  b += align256(sizeof(int64_t) * 2);      // segment count
+  b += align256(sizeof(int64_t) * 4);      // segment count, chunk counter, pool counter
+  b += align256(sizeof(int32_t) * hot_chunks(N));                       // hot-chunk slots
+  b += align256(sizeof(float) * hot_chunks(N) * (max_dim > 0 ? max_dim : 1));  // hot partials
   b += align256(cub_temp_bytes<Key>(N));
   return b;
 }
@@ -696,7 +822,7 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
                         const void* indices, int32_t index_dtype, void* workspace,
                         size_t ws_bytes, int64_t* out_count, neo_error* err, cudaStream_t s) {
   const int64_t N = p.N;
-  if (ws_bytes < workspace_for<Key>(N))
+  if (ws_bytes < workspace_for<Key>(N, p.max_dim))
     return fail(NEO_E_ARG, "neo_tbe_backward: workspace too small");
   unsigned char* w = static_cast<unsigned char*>(workspace);
   Key* k0 = reinterpret_cast<Key*>(w);
@@ -710,7 +836,12 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   int32_t* starts = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * N);
   int64_t* nseg = reinterpret_cast<int64_t*>(w);
-  w += align256(sizeof(int64_t) * 2);
+  w += align256(sizeof(int64_t) * 4);
+  p.chunk_slot = reinterpret_cast<int32_t*>(w);
+  w += align256(sizeof(int32_t) * hot_chunks(N));
+  p.pool = reinterpret_cast<float*>(w);
+  p.pool_cap = hot_chunks(N);
+  w += align256(sizeof(float) * hot_chunks(N) * (p.max_dim > 0 ? p.max_dim : 1));
   void* temp = w;
   size_t temp_bytes = cub_temp_bytes<Key>(N);
 
@@ -736,6 +867,7 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   p.keys = keys;
   p.bags = vbuf.Current();
   p.chunk_counter = nseg + 1;
+  p.pool_counter = reinterpret_cast<unsigned*>(nseg + 2);
   const int wvec = weight_dtype == NEO_F16 ? 8 : 4;
   const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
                     p.max_dim <= kWarp * wvec && !out_count &&
@@ -807,10 +939,10 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
 
 }  // namespace neo
 
-extern "C" size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows) {
+extern "C" size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows, int32_t max_dim) {
   if (num_indices < 1) num_indices = 1;
-  return neo::use_wide_keys(total_rows) ? neo::workspace_for<uint64_t>(num_indices)
-                                        : neo::workspace_for<uint32_t>(num_indices);
+  return neo::use_wide_keys(total_rows) ? neo::workspace_for<uint64_t>(num_indices, max_dim)
+                                        : neo::workspace_for<uint32_t>(num_indices, max_dim);
 }
 
 extern "C" int neo_tbe_backward(int32_t num_tables, int64_t batch, const int64_t* row_offsets,

@@ -72,10 +72,12 @@ class NcclComm(Comm):
         self.bytes_sent = 0
 
     def all_to_all(self, outs, ins, out_splits, in_splits) -> None:
-        out, inp = outs[0], ins[0]
-        self.bytes_sent += (sum(in_splits[0]) - in_splits[0][self.ranks[0]]) * inp.element_size()
-        self.dist.all_to_all_single(out, inp, list(map(int, out_splits[0])), list(map(int, in_splits[0])),
-                                    group=self.group)
+        osp = [int(x) for x in out_splits[0]]
+        isp = [int(x) for x in in_splits[0]]
+        # persistent buffers may be larger than this step's payload
+        out, inp = outs[0][:sum(osp)], ins[0][:sum(isp)]
+        self.bytes_sent += (sum(isp) - isp[self.ranks[0]]) * inp.element_size()
+        self.dist.all_to_all_single(out, inp, osp, isp, group=self.group)
 
     def all_reduce_sum(self, tensors) -> None:
         self.dist.all_reduce(tensors[0], group=self.group)

@@ -244,7 +244,7 @@ class TableGroup:
             ro, total_rows = self.row_offsets, self.total_rows
         if n_idx == 0:
             return
-        ws_bytes = capi.lib().neo_tbe_backward_workspace_bytes(n_idx, total_rows)
+        ws_bytes = capi.lib().neo_tbe_backward_workspace_bytes(n_idx, total_rows, self.max_dim)
         ws = WORKSPACE.get("tbe_bwd", ws_bytes, self.device)
         i8, i4 = 8, 4
         rc = capi.lib().neo_tbe_backward(

@@ -65,6 +65,7 @@ def test_host_side_argument_errors(capi):
 
 def test_workspace_queries_host_only(capi):
     lib = capi.lib()
-    assert lib.neo_tbe_backward_workspace_bytes(1 << 20, 1 << 20) > 5 * (1 << 22)
-    assert lib.neo_tbe_backward_workspace_bytes(1 << 20, 1 << 33) > lib.neo_tbe_backward_workspace_bytes(1 << 20, 1 << 20)
+    assert lib.neo_tbe_backward_workspace_bytes(1 << 20, 1 << 20, 128) > 5 * (1 << 22)
+    assert lib.neo_tbe_backward_workspace_bytes(1 << 20, 1 << 33, 128) > \
+        lib.neo_tbe_backward_workspace_bytes(1 << 20, 1 << 20, 128)
     assert lib.neo_permute_workspace_bytes(8, 64) >= 4 * 8 * 64 * 8

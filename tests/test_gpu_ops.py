@@ -314,3 +314,42 @@ def test_backward_subgroup_split_bitwise(pkg, monkeypatch):
         res.append((grp._storage.cpu(), torch.cat([m.cpu() for m in grp.moments])))
     assert len(grp._sort_groups()) > 1
     assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
+
+
+@pytest.mark.parametrize("dims", [[128, 128], [64, 32]])
+def test_hot_rows_skewed(pkg, dims):
+    """Skewed ids (a few rows hit thousands of times): rows spanning many
+    128-entry chunks are folded from precomputed chunk partials; results
+    stay within the f32 tolerance of the oracle and deterministic."""
+    from paper_2104_05158_b200 import tbe
+
+    rng = np.random.default_rng(9)
+    rows, B, L = [40, 3000], 4096, 24
+    lengths = np.full((2, B), L)
+    # table 0: 40 rows -> ~2500 occurrences each; table 1: Zipf-like
+    p = 1.0 / np.arange(1, rows[1] + 1) ** 1.1
+    p /= p.sum()
+    idx = np.concatenate([rng.integers(0, rows[0], size=B * L), rng.choice(rows[1], size=B * L, p=p)])
+    up = rng.standard_normal((B, sum(dims))).astype(np.float32)
+    res = []
+    for _ in range(2):
+        grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim="rowwise_adagrad")
+        init = [rng.standard_normal((r, d)).astype(np.float32) for r, d in zip(rows, dims)] if not res else init
+        for w, v in zip(grp.weights, init):
+            w.copy_(torch.from_numpy(v))
+        off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+        grp.backward(torch.from_numpy(idx).int().cuda(), off, B, torch.from_numpy(up).cuda(), mode="update",
+                     optim="rowwise_adagrad", lr=0.05, eps=1e-8)
+        res.append([w.double().cpu().numpy() for w in grp.weights])
+    col = 0
+    tab_off = O.offsets_of(lengths.sum(axis=1))
+    for t, D in enumerate(dims):
+        assert np.array_equal(res[0][t], res[1][t])  # deterministic
+        v = init[t].astype(np.float64)
+        part = idx[tab_off[t]:tab_off[t + 1]]
+        ids, g = O.backward_aggregate_c(lengths[t], part, np.ascontiguousarray(up[:, col:col + D].astype(np.float64)))
+        w0 = v.copy()
+        O.apply_c("rowwise_adagrad", v, np.zeros(rows[t]), ids, g, 0.05, 1e-8)
+        tol = 1e-5 * (np.abs(v) + np.abs(v - w0)) + 1e-6
+        assert (np.abs(res[0][t] - v) <= tol).all(), (t, np.abs(res[0][t] - v).max())
+        col += D
