@@ -506,7 +506,10 @@ tbe_stream_update_kernel(SegParams p) {
         int l = pe - (int)(pw.base - c0);
         if (l == kWarp) {  // slide to the next window
           const int64_t nb = pw.base + kWarp;
-          if (nb % kChunk == 0 && nb < p.N && p.chunk_slot[nb / kChunk] >= 0) {
+#ifndef NEO_HOT_CHUNKS
+#define NEO_HOT_CHUNKS 1
+#endif
+          if (NEO_HOT_CHUNKS && nb % kChunk == 0 && nb < p.N && p.chunk_slot[nb / kChunk] >= 0) {
             // the row continues through a hot chunk: its partials are folded in below
             pend = pe;
             cont_chunk = nb / kChunk;
@@ -679,7 +682,7 @@ tbe_stream_update_kernel(SegParams p) {
 #pragma unroll
         for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
       }
-      if (stop) break;
+      if (stop || (pend >= 0 && ce >= pend)) break;  // range may end exactly at a window edge
       cw = pw;  // the producer is already in the next window
     }
     if (cont_chunk >= 0 && cslot >= 0) {

@@ -137,3 +137,51 @@ def test_sharded_f32_engine_matches_oracle(pkg):
             gw = w.double().cpu().numpy()
             base = full[t][r0:r1, c0:c1]
             assert (np.abs(gw - v) <= 1e-5 * (np.abs(v) + np.abs(v - base)) + 1e-6).all(), (s.table_id, s.index)
+
+
+def test_quantized_alltoall_fp16_fwd_bf16_bwd(pkg):
+    """Paper-style quantized communication: pooled rows cross
+    the all-to-all as fp16 (written by the TBE epilogue), gradients as bf16.
+    Received pooled values equal the fp16 rounding of the f32 result
+    (comms oracle: quantize_fp16_roundtrip, embedding.py:288-299); the update
+    sees the bf16-rounded upstream (restated RNE, parity unpinned)."""
+    from oracle import tbe_oracle as O
+    from paper_2104_05158_b200 import dist, plan as P
+    from paper_2104_05158_b200.comms import _local_batches
+
+    rng = np.random.default_rng(4)
+    W, B = 2, 128
+    specs = [pkg.TableSpec(id=f"t{i}", num_rows=2000, dim=128, avg_pooling=8.0) for i in range(3)]
+    model = pkg.ModelSpec(tables=tuple(specs), local_batch=B)
+    plan = P.ShardingPlan(W, W, tuple(P.TableAssignment(t.id, P.Scheme(P.SchemeKind.TABLE_WISE), (P.Shard(i % W),))
+                                      for i, t in enumerate(specs)))
+    full = [rng.standard_normal((2000, 128)).astype(np.float32) for _ in specs]
+    batch = pkg.gen_synthetic_batch(model, W * B, seed=11)
+
+    def run(fwd, bwd):
+        eng = dist.ShardedEmbedding(model, plan, dist.LocalComm(W), B, dtype=torch.float32, optim="sgd",
+                                    fwd_comm=fwd, bwd_comm=bwd,
+                                    init=lambda t, r, c: torch.from_numpy(full[t][r[0]:r[1], c[0]:c[1]].copy()))
+        up = torch.from_numpy(rng.standard_normal((B, 384)).astype(np.float32)).cuda()
+        pooled = [p.clone() for p in eng.step(_local_batches(batch, W), lr=0.1, upstream_fn=lambda p: up)]
+        return eng, torch.cat(pooled).double().cpu().numpy(), up
+
+    eng32, p32, _ = run(None, None)
+    engq, pq, up = run(torch.float16, torch.bfloat16)
+    assert np.array_equal(pq, O.fp16_roundtrip(p32)[0])  # one fp16 rounding of the same f32 sums
+    # the bf16 wire rounds the upstream once: check the SGD update of every shard
+    upb = O.bf16_roundtrip(up.double().cpu().numpy())
+    L = np.asarray(batch.lengths)
+    tab_off = O.offsets_of(L.sum(axis=1))
+    for slot in range(W):
+        for s, w, _ in engq.shard_tensors(slot):
+            t = s.table
+            part = np.asarray(batch.indices)[tab_off[t]:tab_off[t + 1]]
+            ups = np.concatenate([upb] * W)[:, 128 * t:128 * (t + 1)]  # every worker used the same upstream
+            ids, g = O.backward_aggregate_c(L[t], part, np.ascontiguousarray(ups))
+            v = full[t].astype(np.float64)
+            O.apply_c("sgd", v, None, ids, g, 0.1, 0.0)
+            got = w.double().cpu().numpy()
+            assert (np.abs(got - v) <= 1e-5 * (np.abs(v) + np.abs(v - full[t])) + 1e-6).all()
+    # byte contract: fp16 payload is exactly half of fp32 (criterion 8, test_acceptance.py:318-343)
+    assert engq.pooled_send_bytes(0) * 2 == eng32.pooled_send_bytes(0)
