@@ -405,8 +405,9 @@ def run_sharded(a, rank, world, dev):
                               index_dtype=torch.int32)
     torch.manual_seed(rank)
     for st in eng.states:
-        if st.group is not None:
-            st.group._storage.normal_()
+        for grp in st.groups:
+            if grp is not None:
+                grp._storage.normal_()
     lengths = np.full((T, B), L, dtype=np.int64)
     L_dev = torch.full((T * B,), L, dtype=torch.int64, device=dev)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
@@ -440,6 +441,7 @@ def run_sharded(a, rank, world, dev):
                       ph.get("a2a_bwd", 0.0)], dtype=torch.float64, device=dev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms, fwd_ms, bwd_ms, a2f_ms, a2b_ms = t.tolist()
+    busbw = alltoall_busbw(eng, dev, world)
     # per-rank algorithmic bytes of the local TBE (max over ranks of local tables)
     T_loc = max(len(eng.lay.owned[v]) for v in range(world))
     n = B * world
@@ -465,10 +467,12 @@ def run_sharded(a, rank, world, dev):
         "roofline": {"bound": "hbm", "kernel": "tbe_forward_kernel (local shards)", "achieved": fwd_gbs, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak, "traffic": None,
                      "algorithmic_bytes": fb, "ms": fwd_ms},
-        "phases_ms": {"fwd": fwd_ms, "bwd": bwd_ms, "a2a_fwd": a2f_ms, "a2a_bwd": a2b_ms},
-        "alltoall": {"send_bytes_per_gpu": send, "fwd_busbw_gbs": send / (a2f_ms * 1e-3) / 1e9,
-                     "bwd_busbw_gbs": send / (a2b_ms * 1e-3) / 1e9, "peak_gbs": 900.0,
-                     "note": "per-GPU send bytes excluding self (comms.py:366-392) / all_to_all time"},
+        "phases_ms": {"fwd_incl_overlapped_a2a": fwd_ms, "a2a_fwd_tail": a2f_ms,
+                      "bwd_incl_overlapped_a2a": bwd_ms, "overlap_groups": eng.G},
+        "alltoall": {"send_bytes_per_gpu": send, "busbw_gbs": busbw["busbw_gbs"], "ms": busbw["ms"],
+                     "peak_gbs": 900.0, "frac_of_nominal": busbw["busbw_gbs"] / 900.0,
+                     "note": "pooled all-to-all payload of one step (per-GPU send bytes excluding self, "
+                             "comms.py:366-392) timed standalone with CUDA events, max over ranks"},
         "roofline_bwd": {"achieved": bb / (bwd_ms * 1e-3) / 1e9, "bytes_expected_U": bb, "ms": bwd_ms},
         "gpu_launches": launches_per_step * a.steps,
         "clocks": clk,
@@ -477,6 +481,36 @@ def run_sharded(a, rank, world, dev):
         line["e2e"] = e2e
     print(json.dumps(line), flush=True)
     tdist.destroy_process_group()
+
+
+def alltoall_busbw(eng, dev, world) -> dict:
+    """Pooled all-to-all bus bandwidth at this step's payload: per-GPU bytes
+    sent to other GPUs / time (nccl-tests alltoall busbw definition)."""
+    import torch
+    import torch.distributed as tdist
+
+    rank = tdist.get_rank()
+    B = eng.B
+    per_peer = B * eng.widths[rank]
+    send = torch.empty(per_peer * world, dtype=eng.fwd_comm, device=dev)
+    recv = torch.empty(sum(B * eng.widths[w] for w in range(world)), dtype=eng.fwd_comm, device=dev)
+    osp = [B * eng.widths[w] for w in range(world)]
+    for _ in range(3):
+        tdist.all_to_all_single(recv, send, osp, [per_peer] * world)
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record()
+    for _ in range(reps):
+        tdist.all_to_all_single(recv, send, osp, [per_peer] * world)
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    nbytes = per_peer * (world - 1) * send.element_size()
+    return {"ms": ms, "busbw_gbs": nbytes / (ms * 1e-3) / 1e9}
 
 
 def e2e_sharded(a, eng, rank, world, dev, lengths, L_dev) -> dict:

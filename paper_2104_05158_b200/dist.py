@@ -52,7 +52,8 @@ class Comm:
     world: int
     ranks: list
 
-    def all_to_all(self, outs, ins, out_splits, in_splits) -> None:  # pragma: no cover
+    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False):  # pragma: no cover
+        """Returns a handle with .wait() when async_op (None otherwise)."""
         raise NotImplementedError
 
     def all_reduce_sum(self, tensors) -> None:  # pragma: no cover
@@ -71,13 +72,13 @@ class NcclComm(Comm):
         self.ranks = [dist.get_rank(group)]
         self.bytes_sent = 0
 
-    def all_to_all(self, outs, ins, out_splits, in_splits) -> None:
+    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False):
         osp = [int(x) for x in out_splits[0]]
         isp = [int(x) for x in in_splits[0]]
         # persistent buffers may be larger than this step's payload
         out, inp = outs[0][:sum(osp)], ins[0][:sum(isp)]
         self.bytes_sent += (sum(isp) - isp[self.ranks[0]]) * inp.element_size()
-        self.dist.all_to_all_single(out, inp, osp, isp, group=self.group)
+        return self.dist.all_to_all_single(out, inp, osp, isp, group=self.group, async_op=async_op)
 
     def all_reduce_sum(self, tensors) -> None:
         self.dist.all_reduce(tensors[0], group=self.group)
@@ -93,7 +94,7 @@ class LocalComm(Comm):
         self.ranks = list(range(world))
         self.bytes_sent = 0
 
-    def all_to_all(self, outs, ins, out_splits, in_splits) -> None:
+    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False):
         W = self.world
         ioff = [np.concatenate(([0], np.cumsum(s)))[:-1] for s in in_splits]
         ooff = [np.concatenate(([0], np.cumsum(s)))[:-1] for s in out_splits]
@@ -122,7 +123,8 @@ class LocalComm(Comm):
 @dataclass
 class RankState:
     rank: int
-    group: Optional[tbe.TableGroup] = None       # local TW/RW/CW shards
+    group: Optional[tbe.TableGroup] = None       # first non-empty local group (None: no shards)
+    groups: list = field(default_factory=list)   # local TW/RW/CW shards, one TableGroup per overlap group
     dp_group: Optional[tbe.TableGroup] = None    # replicated DP tables
     dp_dense: Optional[torch.Tensor] = None      # flat dense DP gradient buffer
     dp_dense_views: list = field(default_factory=list)
@@ -150,7 +152,7 @@ class ShardedEmbedding:
     def __init__(self, model, plan, comm: Comm, local_batch: int, device=None, dtype=torch.float32,
                  optim: str = "rowwise_adagrad", fwd_comm: Optional[torch.dtype] = None,
                  bwd_comm: Optional[torch.dtype] = None, index_dtype=torch.int64,
-                 init: Optional[Callable] = None):
+                 init: Optional[Callable] = None, overlap_groups: int = 4):
         self.model = model
         self.lay: RankLayout = rank_layout(model, plan)
         if self.lay.world != comm.world:
@@ -169,6 +171,25 @@ class ShardedEmbedding:
         self.T = len(model.tables)
         lay = self.lay
         self.widths = [lay.width(w) for w in range(self.W)]
+        # Local shards are split into G groups (same G on every rank: each group
+        # is one all-to-all); group g's pooled rows form their own contiguous
+        # block, so its exchange overlaps the TBE of group g+1 (and, backward,
+        # the exchange of group g+1 overlaps the fused update of group g).
+        from .plan import even_bounds
+
+        self.G = max(1, min(overlap_groups, max(len(lay.owned[v]) for v in range(self.W)) or 1))
+        self.gbounds, self.gwidth = [], []
+        for v in range(self.W):
+            bounds = even_bounds(len(lay.owned[v]), self.G) if lay.owned[v] else [(0, 0)] * self.G
+            widths = []
+            for g, (k0, k1) in enumerate(bounds):
+                c = 0
+                for s_ in lay.owned[v][k0:k1]:
+                    s_.grp, s_.out_col = g, c
+                    c += s_.dim
+                widths.append(c)
+            self.gbounds.append(bounds)
+            self.gwidth.append(widths)
         # send order of input blocks: destination-major, then the destination's shards
         self.send_blocks = [(v, s) for v in range(self.W) for s in lay.owned[v]]
         self.rw_slot = {}
@@ -187,14 +208,19 @@ class ShardedEmbedding:
     def _make_state(self, r: int, init) -> RankState:
         lay = self.lay
         st = RankState(rank=r)
-        shards = lay.owned[r]
-        if shards:
-            st.group = tbe.TableGroup([s.num_rows for s in shards], [s.dim for s in shards], dtype=self.dtype,
-                                      optim=self.optim, device=self.device,
-                                      table_ids=[f"{s.table_id}#{s.index}" for s in shards])
+        for (k0, k1) in self.gbounds[r]:
+            shards = lay.owned[r][k0:k1]
+            if not shards:
+                st.groups.append(None)
+                continue
+            grp = tbe.TableGroup([s.num_rows for s in shards], [s.dim for s in shards], dtype=self.dtype,
+                                 optim=self.optim, device=self.device,
+                                 table_ids=[f"{s.table_id}#{s.index}" for s in shards])
             if init is not None:
-                for s, w in zip(shards, st.group.weights):
+                for s, w in zip(shards, grp.weights):
                     w.copy_(init(s.table, s.rows, s.cols).to(w.dtype))
+            st.groups.append(grp)
+        st.group = next((g for g in st.groups if g is not None), None)
         if lay.dp_tables:
             st.dp_group = tbe.TableGroup([lay.rows[t] for t in lay.dp_tables], [lay.dims[t] for t in lay.dp_tables],
                                          dtype=self.dtype, optim=self.optim, device=self.device,
@@ -266,18 +292,26 @@ class ShardedEmbedding:
         local rank (model table order).  upstream_fn(pooled) -> gradient
         (default: ones, the reference's sum-of-outputs loss).  timers: dict
         receiving CUDA event pairs for "fwd", "a2a_fwd", "a2a_bwd", "bwd"."""
-        W = self.W
+        W, B = self.W, self.B
         S = self.states
         ev = _Timers(timers)
         self._exchange_inputs(batches)
         ev.start("fwd")
         for st in S:
-            self._forward_local(st)
+            self._prepare_forward(st)
+        handles = []
+        for g in range(self.G):  # TBE of group g, then its exchange (async) while group g+1 computes
+            for st in S:
+                self._forward_group(st, g)
+            handles.append(self.comm.all_to_all(
+                [st.sc["recv_pool"][g] for st in S], [st.sc["send_pool"][g] for st in S],
+                [[B * self.gwidth[w][g] for w in range(W)] for st in S],
+                [[B * self.gwidth[st.rank][g]] * W for st in S], async_op=True))
         ev.stop("fwd")
         ev.start("a2a_fwd")
-        self.comm.all_to_all([st.sc["recv_pool"] for st in S], [st.sc["send_pool"] for st in S],
-                             [[self.B * wd for wd in self.widths] for st in S],
-                             [[self.B * self.widths[st.rank]] * W for st in S])
+        for h in handles:
+            if h is not None:
+                h.wait()
         ev.stop("a2a_fwd")
         pooled = [self._assemble(st) for st in S]
         for st, p in zip(S, pooled):
@@ -289,14 +323,18 @@ class ShardedEmbedding:
                     g.fill_(1.0)
                     st.cache["ones_ready"] = g.data_ptr()
             self._pack_grad(st, g)
-        ev.start("a2a_bwd")
-        self.comm.all_to_all([st.sc["recv_grad"] for st in S], [st.sc["send_grad"] for st in S],
-                             [[self.B * self.widths[st.rank]] * W for st in S],
-                             [[self.B * wd for wd in self.widths] for st in S])
-        ev.stop("a2a_bwd")
         ev.start("bwd")
+        handles = [self.comm.all_to_all(
+            [st.sc["recv_grad"][g] for st in S], [st.sc["send_grad"][g] for st in S],
+            [[B * self.gwidth[st.rank][g]] * W for st in S],
+            [[B * self.gwidth[v][g] for v in range(W)] for st in S], async_op=True) for g in range(self.G)]
+        for g, h in enumerate(handles):  # update of group g while group g+1's gradients arrive
+            if h is not None:
+                h.wait()
+            for st in S:
+                self._backward_group(st, g, lr, eps)
         for st in S:
-            self._backward_local(st, lr, eps)
+            self._backward_dp(st)
         ev.stop("bwd")
         if self.lay.dp_tables:
             self.comm.all_reduce_sum([st.dp_dense for st in S])
@@ -439,16 +477,16 @@ class ShardedEmbedding:
         off = tbe.lengths_to_offsets(perm_len)
         return perm_len, perm_ids, off
 
-    def _forward_local(self, st: RankState) -> None:
+    def _prepare_forward(self, st: RankState) -> None:
         W, B, n = self.W, self.B, self.n
         sc = st.sc
-        width = self.widths[st.rank]
-        sc["send_pool"] = self._buf(st, "send_pool", n * width, self.fwd_comm)
-        sc["recv_pool"] = self._buf(st, "recv_pool", B * sum(self.widths), self.fwd_comm)
+        sc["send_pool"] = [self._buf(st, f"send_pool{g}", n * self.gwidth[st.rank][g], self.fwd_comm)
+                           for g in range(self.G)]
+        sc["recv_pool"] = [self._buf(st, f"recv_pool{g}", B * sum(self.gwidth[w][g] for w in range(W)),
+                                     self.fwd_comm) for g in range(self.G)]
         if st.group is not None:
             _, perm_ids, off = self._permute_local(st)
             sc["perm_ids"], sc["perm_off"] = perm_ids, off
-            st.group.forward(perm_ids, off, n, out=sc["send_pool"][:n * width].view(n, width))
         if st.dp_group is not None:  # data-parallel tables: local batch only
             ids, tab_off, L_dev = sc["ids"], sc["tab_off"], sc["L_dev"]
             dp = self.lay.dp_tables
@@ -461,19 +499,32 @@ class ShardedEmbedding:
             dp_out = self._buf(st, "dp_out", B * self.dp_width, self.acc)[:B * self.dp_width].view(B, self.dp_width)
             sc["dp_out"] = st.dp_group.forward(dp_ids, sc["dp_off"], B, out=dp_out)
 
+    def _forward_group(self, st: RankState, g: int) -> None:
+        grp = st.groups[g] if st.groups else None
+        if grp is None:
+            return
+        n = self.n
+        k0, _ = self.gbounds[st.rank][g]
+        gw = self.gwidth[st.rank][g]
+        sc = st.sc
+        grp.forward(sc["perm_ids"], sc["perm_off"][k0 * n:], n, out=sc["send_pool"][g][:n * gw].view(n, gw))
+
     def _assemble(self, st: RankState) -> torch.Tensor:
         """Place received column blocks (TW copy, CW column placement, RW
         partial sums in shard order: comms.py:692-711) in model order."""
         lay, W, B = self.lay, self.W, self.B
         sc = st.sc
         pooled = self._buf(st, "pooled", B * lay.total_dim, self.acc)[:B * lay.total_dim].view(B, lay.total_dim)
-        key = ("asm", sc["recv_pool"].data_ptr(), pooled.data_ptr(),
+        key = ("asm", tuple(b.data_ptr() for b in sc["recv_pool"]), pooled.data_ptr(),
                sc["dp_out"].data_ptr() if "dp_out" in sc else 0)
         packed = st.cache.get(key)
         if packed is None:
-            starts = np.concatenate(([0], np.cumsum([B * wd for wd in self.widths])))
-            views = [sc["recv_pool"][int(starts[w]):int(starts[w + 1])].view(B, self.widths[w])
-                     if self.widths[w] else None for w in range(W)]
+            views = {}
+            for g in range(self.G):
+                starts = np.concatenate(([0], np.cumsum([B * self.gwidth[w][g] for w in range(W)])))
+                for w in range(W):
+                    if self.gwidth[w][g]:
+                        views[(w, g)] = sc["recv_pool"][g][int(starts[w]):int(starts[w + 1])].view(B, self.gwidth[w][g])
             where = {(s.table, s.index): (w, s) for w in range(W) for s in lay.owned[w]}
             pieces, dp_pieces = [], []
             for t in range(self.T):
@@ -482,8 +533,8 @@ class ShardedEmbedding:
                     continue
                 for k, i in enumerate(sorted(i for (tt, i) in where if tt == t)):
                     w, s = where[(t, i)]
-                    pieces.append(tbe.Piece(views[w], pooled, s.out_col, lay.model_cols[t] + s.cols[0], s.dim,
-                                            s.kind == "row_wise" and k > 0))
+                    pieces.append(tbe.Piece(views[(w, s.grp)], pooled, s.out_col, lay.model_cols[t] + s.cols[0],
+                                            s.dim, s.kind == "row_wise" and k > 0))
             packed = [(pl, tbe.pack_pieces(pl, self.device) if pl else None) for pl in (pieces, dp_pieces)]
             st.cache[key] = packed
         for pl, dev_tab in packed:
@@ -492,28 +543,32 @@ class ShardedEmbedding:
         return pooled
 
     def _pack_grad(self, st: RankState, grad: torch.Tensor) -> None:
-        lay, W, B = self.lay, self.W, self.B
+        lay, W, B, n = self.lay, self.W, self.B, self.n
         sc = st.sc
         grad = grad.contiguous()
-        send = self._buf(st, "send_grad", B * sum(self.widths), self.bwd_comm)
-        me = self.widths[st.rank]
-        sc["send_grad"] = send
-        sc["recv_grad"] = self._buf(st, "recv_grad", self.n * me, self.bwd_comm)
+        sends = [self._buf(st, f"send_grad{g}", B * sum(self.gwidth[v][g] for v in range(W)), self.bwd_comm)
+                 for g in range(self.G)]
+        sc["send_grad"] = sends
+        sc["recv_grad"] = [self._buf(st, f"recv_grad{g}", n * self.gwidth[st.rank][g], self.bwd_comm)
+                           for g in range(self.G)]
         g_dp = None
         if st.dp_group is not None:
             g_dp = self._buf(st, "dp_grad", B * self.dp_width, self.acc)[:B * self.dp_width].view(B, self.dp_width)
             sc["dp_grad"] = g_dp
-        key = ("grad", grad.data_ptr(), send.data_ptr(), 0 if g_dp is None else g_dp.data_ptr())
+        key = ("grad", grad.data_ptr(), tuple(x.data_ptr() for x in sends), 0 if g_dp is None else g_dp.data_ptr())
         packed = st.cache.get(key)
         if packed is None:
-            starts = np.concatenate(([0], np.cumsum([B * wd for wd in self.widths])))
             pieces = []
-            for v in range(W):
-                if not self.widths[v]:
-                    continue
-                chunk = send[int(starts[v]):int(starts[v + 1])].view(B, self.widths[v])
-                for s in lay.owned[v]:
-                    pieces.append(tbe.Piece(grad, chunk, lay.model_cols[s.table] + s.cols[0], s.out_col, s.dim))
+            for g in range(self.G):
+                starts = np.concatenate(([0], np.cumsum([B * self.gwidth[v][g] for v in range(W)])))
+                for v in range(W):
+                    gw = self.gwidth[v][g]
+                    if not gw:
+                        continue
+                    chunk = sends[g][int(starts[v]):int(starts[v + 1])].view(B, gw)
+                    k0, k1 = self.gbounds[v][g]
+                    for s in lay.owned[v][k0:k1]:
+                        pieces.append(tbe.Piece(grad, chunk, lay.model_cols[s.table] + s.cols[0], s.out_col, s.dim))
             dp_pieces = [tbe.Piece(grad, g_dp, lay.model_cols[t], self.dp_cols[t], lay.dims[t])
                          for t in lay.dp_tables] if g_dp is not None else []
             packed = [(pl, tbe.pack_pieces(pl, self.device) if pl else None) for pl in (pieces, dp_pieces)]
@@ -524,13 +579,19 @@ class ShardedEmbedding:
             if pl:
                 tbe.copy_pieces(B, pl, dev_tab)
 
-    def _backward_local(self, st: RankState, lr: float, eps: float) -> None:
+    def _backward_group(self, st: RankState, g: int, lr: float, eps: float) -> None:
+        grp = st.groups[g] if st.groups else None
+        if grp is None:
+            return
+        n = self.n
         sc = st.sc
-        if st.group is not None:
-            me = self.widths[st.rank]
-            g = sc["recv_grad"][:self.n * me].view(self.n, me)
-            st.group.backward(sc["perm_ids"], sc["perm_off"], self.n, g, mode="update", optim=self.optim,
-                              lr=lr, eps=eps, table_counts=sc["shard_counts"])
+        k0, k1 = self.gbounds[st.rank][g]
+        gw = self.gwidth[st.rank][g]
+        grp.backward(sc["perm_ids"], sc["perm_off"][k0 * n:], n, sc["recv_grad"][g][:n * gw].view(n, gw),
+                     mode="update", optim=self.optim, lr=lr, eps=eps, table_counts=sc["shard_counts"][k0:k1])
+
+    def _backward_dp(self, st: RankState) -> None:
+        sc = st.sc
         if st.dp_group is not None:
             st.dp_dense.zero_()
             st.dp_group.backward(sc["dp_ids"], sc["dp_off"], self.B, sc["dp_grad"], mode="dense",
@@ -544,9 +605,11 @@ class ShardedEmbedding:
     def shard_tensors(self, rank_slot: int = 0):
         """[(LocalShard, weight, moment)] of a local rank."""
         st = self.states[rank_slot]
-        if st.group is None:
-            return []
-        return list(zip(self.lay.owned[st.rank], st.group.weights, st.group.moments))
+        out = []
+        for (k0, k1), grp in zip(self.gbounds[st.rank], st.groups):
+            if grp is not None:
+                out += list(zip(self.lay.owned[st.rank][k0:k1], grp.weights, grp.moments))
+        return out
 
 
 class _Timers:
