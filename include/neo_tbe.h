@@ -127,6 +127,7 @@ int neo_tbe_forward(int32_t num_tables, int64_t batch,
  *         (U x max_dim, accumulator type), *out_count = U (device int64)
  *   DENSE: dense_grads[t] (H_t x D_t, accumulator type, pre-zeroed) get the
  *         aggregated rows.
+ * num_indices must equal offsets[T*B] - offsets[0] (the ids the bags cover).
  * Workspace size: neo_tbe_backward_workspace_bytes. */
 size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows, int32_t max_dim);
 

@@ -496,6 +496,7 @@ class ShardedEmbedding:
             dp_len = self._buf(st, "dp_len", len(dp) * B, torch.int64)[:len(dp) * B]
             tbe.gather_blocks([L_dev[t * B:(t + 1) * B] for t in dp], [B] * len(dp), dp_len)
             sc["dp_ids"], sc["dp_off"] = dp_ids, tbe.lengths_to_offsets(dp_len)
+            sc["dp_counts"] = cnts  # exact id counts: dp_ids is a grow-only buffer
             dp_out = self._buf(st, "dp_out", B * self.dp_width, self.acc)[:B * self.dp_width].view(B, self.dp_width)
             sc["dp_out"] = st.dp_group.forward(dp_ids, sc["dp_off"], B, out=dp_out)
 
@@ -595,7 +596,7 @@ class ShardedEmbedding:
         if st.dp_group is not None:
             st.dp_dense.zero_()
             st.dp_group.backward(sc["dp_ids"], sc["dp_off"], self.B, sc["dp_grad"], mode="dense",
-                                 dense_grads=st.dp_dense_views)
+                                 dense_grads=st.dp_dense_views, table_counts=sc["dp_counts"])
 
     def _dp_update(self, st: RankState, lr: float, eps: float) -> None:
         for w, m, g in zip(st.dp_group.weights, st.dp_group.moments, st.dp_dense_views):

@@ -177,8 +177,10 @@ class TableGroup:
         (in place); "aggregate": returns (ids, grads, count) with global row
         keys; "dense": accumulates into dense_grads (per table, pre-zeroed).
         table_counts: optional host per-table id counts; lets an UPDATE over
-        more than 2^SORT_BITS rows run as sub-groups with shorter sort keys."""
-        n_idx = int(indices.numel())
+        more than 2^SORT_BITS rows run as sub-groups with shorter sort keys.
+        The ids covered are offsets[0] .. offsets[T*batch]; indices may be a
+        larger buffer, so its length is only used when table_counts is None."""
+        n_idx = int(indices.numel()) if table_counts is None else int(sum(table_counts))
         out_ids = out_grads = out_count = None
         dense_ptrs = None
         mode_code = {"update": capi.NEO_BWD_UPDATE, "aggregate": capi.NEO_BWD_AGGREGATE,
