@@ -74,6 +74,12 @@ enum {
  *          and the gradient (base, stride, column offsets) are 16-byte aligned;
  * FULL_ROWS: additionally every D equals 32 vectors (128 f32 / 256 f16). */
 enum { NEO_BWD_FLAG_ALIGNED = 0x100, NEO_BWD_FLAG_FULL_ROWS = 0x200 };
+/* optional phase split of an UPDATE on the streamed path (same arguments
+ * and workspace for both calls): PREPARE builds and sorts the (row, bag)
+ * pairs; APPLY (later, possibly on another stream once PREPARE's work is
+ * ordered before it) runs the segment walk + optimizer.  Lets the sort of
+ * one table group overlap the update of another. */
+enum { NEO_BWD_FLAG_PREPARE = 0x400, NEO_BWD_FLAG_APPLY = 0x800 };
 
 /* Device-side error record (caller allocates sizeof(neo_error) bytes of
  * device memory).  position = first offending position in index-buffer
@@ -113,6 +119,20 @@ int neo_tbe_forward(int32_t num_tables, int64_t batch,
                     void* out, int32_t out_dtype, int64_t out_stride,
                     neo_error* err,              /* may be NULL */
                     void* stream);
+
+/* Same, with the pooled all-to-all fused into the store: bag row b (of the
+ * batch rows) is written to out_ptrs[b / rows_per_dst] at row b %
+ * rows_per_dst (out_ptrs: device array of destination base pointers, e.g.
+ * peer GPUs' symmetric receive buffers mapped over NVLink; comms.py:366-392
+ * pooled AlltoAll). */
+int neo_tbe_forward_scatter(int32_t num_tables, int64_t batch,
+                            const int64_t* row_offsets, const int32_t* dim_offsets, int32_t max_dim,
+                            const uint64_t* weights, int32_t weight_dtype,
+                            const void* indices, int32_t index_dtype,
+                            const int64_t* offsets, int32_t pooling,
+                            const uint64_t* out_ptrs, int64_t rows_per_dst,
+                            int32_t out_dtype, int64_t out_stride,
+                            neo_error* err, void* stream);
 
 /* ---- TBE backward (embedding.py:175-281) ------------------------------
  * Sort (table row, bag) pairs stably by row, run-length segment them, then

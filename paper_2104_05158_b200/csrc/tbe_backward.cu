@@ -26,6 +26,8 @@
 // pairwise order for the row mean and no FMA contraction, so results are
 // bit-identical to the reference.
 #include <climits>
+#include <mutex>
+#include <unordered_map>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -782,6 +784,11 @@ static size_t cub_temp_bytes(int64_t N) {
 
 static inline int64_t hot_chunks(int64_t N) { return (N + 127) / 128; }
 
+// PREPARE/APPLY split: which half of the double buffer holds the sorted
+// pairs of a prepared workspace (host-side; no device sync)
+static std::mutex g_prep_mu;
+static std::unordered_map<const void*, int> g_prep_sel;
+
 template <typename Key>
 static size_t workspace_for(int64_t N, int64_t max_dim) {
   size_t b = 0;
@@ -848,6 +855,24 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   void* temp = w;
   size_t temp_bytes = cub_temp_bytes<Key>(N);
 
+  const bool prepare_only = (p.flags & NEO_BWD_FLAG_PREPARE) != 0;
+  const bool apply_only = (p.flags & NEO_BWD_FLAG_APPLY) != 0;
+  const int wvec = weight_dtype == NEO_F16 ? 8 : 4;
+  const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
+                    p.max_dim <= kWarp * wvec && !out_count &&
+                    p.B * p.grad_stride < (int64_t(1) << 32);  // 32-bit upstream offsets
+  if ((prepare_only || apply_only) && !fast)
+    return fail(NEO_E_ARG, "neo_tbe_backward: PREPARE/APPLY need the streamed UPDATE path");
+  int rc = NEO_OK;
+  cub::DoubleBuffer<Key> kbuf(k0, k1);
+  cub::DoubleBuffer<int32_t> vbuf(v0, v1);
+  if (apply_only) {
+    std::lock_guard<std::mutex> lk(g_prep_mu);
+    auto it = g_prep_sel.find(workspace);
+    if (it == g_prep_sel.end()) return fail(NEO_E_ARG, "neo_tbe_backward: APPLY on an unprepared workspace");
+    kbuf.selector = vbuf.selector = it->second;
+    g_prep_sel.erase(it);
+  } else {
   const int64_t bags = (int64_t)p.T * p.B;
   const unsigned kb_blocks = (unsigned)((bags + 7) / 8);
   const Key sentinel = (Key)p.total_rows;
@@ -857,24 +882,25 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   else
     build_keys_kernel<int64_t, Key><<<kb_blocks, 256, 0, s>>>(
         p.T, p.B, p.row_offsets, (const int64_t*)indices, p.offsets, k0, v0, sentinel, err);
-  int rc = check_launch("neo_tbe_backward(keys)");
+  rc = check_launch("neo_tbe_backward(keys)");
   if (rc) return rc;
 
-  cub::DoubleBuffer<Key> kbuf(k0, k1);
-  cub::DoubleBuffer<int32_t> vbuf(v0, v1);
   const int bits = key_bits_for(p.total_rows);
   if (cub::DeviceRadixSort::SortPairs(temp, temp_bytes, kbuf, vbuf, (int)N, 0, bits, s) !=
       cudaSuccess)
     return fail(NEO_E_CUDA, "neo_tbe_backward: radix sort failed");
+  if (prepare_only) {
+    std::lock_guard<std::mutex> lk(g_prep_mu);
+    g_prep_sel[workspace] = kbuf.selector;
+    launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
+    return check_launch("neo_tbe_backward(prepare)");
+  }
+  }  // !apply_only
   const Key* keys = kbuf.Current();
   p.keys = keys;
   p.bags = vbuf.Current();
   p.chunk_counter = nseg + 1;
   p.pool_counter = reinterpret_cast<unsigned*>(nseg + 2);
-  const int wvec = weight_dtype == NEO_F16 ? 8 : 4;
-  const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
-                    p.max_dim <= kWarp * wvec && !out_count &&
-                    p.B * p.grad_stride < (int64_t(1) << 32);  // 32-bit upstream offsets
   if (fast) {
     const bool h = weight_dtype == NEO_F16;
     switch (grad_dtype) {
@@ -892,7 +918,7 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
         return fail(NEO_E_ARG, "neo_tbe_backward: gradient dtype must be F32, BF16 or F16");
     }
     if (rc) return rc;
-    launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
+    if (!apply_only) launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
     return check_launch("neo_tbe_backward(finalize)");
   }
   cub::CountingInputIterator<int32_t> it(0);

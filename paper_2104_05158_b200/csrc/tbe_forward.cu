@@ -23,6 +23,10 @@
 namespace neo {
 
 constexpr int kFwdWarps = 8;   // warps per CTA
+// scatter destination of the current launch (set by neo_tbe_forward_scatter
+// around the dispatch; host-side, per thread)
+static thread_local const uint64_t* g_out_ptrs = nullptr;
+static thread_local int64_t g_rows_per_dst = 1;
 constexpr int kFwdStage = 64;  // row ids staged per warp per pass
 constexpr int kFwdUnroll = 8;  // row gathers in flight per lane
 
@@ -110,7 +114,8 @@ __global__ void __launch_bounds__(kFwdWarps * kWarp)
 tbe_forward_kernel(int32_t T, int64_t B, const int64_t* __restrict__ row_offsets,
                    const int32_t* __restrict__ dim_offsets, const uint64_t* __restrict__ weights,
                    const Idx* __restrict__ indices, const int64_t* __restrict__ offsets,
-                   int pooling, Out* __restrict__ out, int64_t out_stride, neo_error* err) {
+                   int pooling, Out* __restrict__ out, int64_t out_stride, neo_error* err,
+                   const uint64_t* __restrict__ out_ptrs, int64_t rows_per_dst) {
   constexpr int kVec = 16 / sizeof(W);
   __shared__ Idx s_idx[kFwdWarps][kFwdStage];
   const int warp = threadIdx.x / kWarp;
@@ -123,10 +128,19 @@ tbe_forward_kernel(int32_t T, int64_t B, const int64_t* __restrict__ row_offsets
   const int32_t D = dim_offsets[t + 1] - doff;
   const int64_t H = row_offsets[t + 1] - row_offsets[t];
   const W* wt = reinterpret_cast<const W*>(weights[t]);
-  Out* orow = out + b * out_stride + doff;
+  // out_ptrs: row b goes to destination b / rows_per_dst (e.g. the peer GPU's
+  // receive buffer: the pooled all-to-all is performed by this store)
+  Out* obase = out;
+  int64_t orow_i = b;
+  if (out_ptrs) {
+    const int64_t d = b / rows_per_dst;
+    obase = reinterpret_cast<Out*>(out_ptrs[d]);
+    orow_i = b - d * rows_per_dst;
+  }
+  Out* orow = obase + orow_i * out_stride + doff;
   const bool vec = (D % kVec) == 0 && aligned16(wt) && (doff % kVec) == 0 &&
                    (out_stride % kVec) == 0 &&
-                   ((reinterpret_cast<uintptr_t>(out) % (sizeof(Out) * kVec)) == 0);
+                   ((reinterpret_cast<uintptr_t>(obase) % (sizeof(Out) * kVec)) == 0);
   if (vec)
     fwd_bag<W, Idx, Out, kVec>(wt, D, H, indices, offsets[bag], offsets[bag + 1], s_idx[warp],
                                pooling, orow, err, lane);
@@ -140,7 +154,7 @@ static int launch_fwd(dim3 grid, cudaStream_t s, int32_t T, int64_t B, const int
                       const int32_t* dof, const uint64_t* w, const void* idx, const int64_t* off,
                       int pooling, void* out, int64_t os, neo_error* err) {
   tbe_forward_kernel<W, Idx, Out><<<grid, kFwdWarps * kWarp, 0, s>>>(
-      T, B, ro, dof, w, (const Idx*)idx, off, pooling, (Out*)out, os, err);
+      T, B, ro, dof, w, (const Idx*)idx, off, pooling, (Out*)out, os, err, g_out_ptrs, g_rows_per_dst);
   return check_launch("neo_tbe_forward");
 }
 
@@ -227,4 +241,26 @@ extern "C" int neo_tbe_forward(int32_t num_tables, int64_t batch, const int64_t*
   if (rc != NEO_OK) return rc;
   launch_error_finalize(err, indices, index_dtype, offsets, batch, num_tables, s);
   return check_launch("neo_tbe_forward(finalize)");
+}
+
+extern "C" int neo_tbe_forward_scatter(int32_t num_tables, int64_t batch, const int64_t* row_offsets,
+                                       const int32_t* dim_offsets, int32_t max_dim,
+                                       const uint64_t* weights, int32_t weight_dtype,
+                                       const void* indices, int32_t index_dtype,
+                                       const int64_t* offsets, int32_t pooling,
+                                       const uint64_t* out_ptrs, int64_t rows_per_dst,
+                                       int32_t out_dtype, int64_t out_stride, neo_error* err,
+                                       void* stream) {
+  using namespace neo;
+  if (!out_ptrs || rows_per_dst < 1)
+    return fail(NEO_E_ARG, "neo_tbe_forward_scatter: out_ptrs and rows_per_dst >= 1 required");
+  g_out_ptrs = out_ptrs;
+  g_rows_per_dst = rows_per_dst;
+  // `out` is unused when out_ptrs is set; pass a non-null placeholder
+  const int rc = neo_tbe_forward(num_tables, batch, row_offsets, dim_offsets, max_dim, weights,
+                                 weight_dtype, indices, index_dtype, offsets, pooling,
+                                 const_cast<uint64_t*>(out_ptrs), out_dtype, out_stride, err, stream);
+  g_out_ptrs = nullptr;
+  g_rows_per_dst = 1;
+  return rc;
 }

@@ -152,7 +152,7 @@ class ShardedEmbedding:
     def __init__(self, model, plan, comm: Comm, local_batch: int, device=None, dtype=torch.float32,
                  optim: str = "rowwise_adagrad", fwd_comm: Optional[torch.dtype] = None,
                  bwd_comm: Optional[torch.dtype] = None, index_dtype=torch.int64,
-                 init: Optional[Callable] = None, overlap_groups: int = 4):
+                 init: Optional[Callable] = None, overlap_groups: int = 4, transport: str = "nccl"):
         self.model = model
         self.lay: RankLayout = rank_layout(model, plan)
         if self.lay.world != comm.world:
@@ -203,6 +203,18 @@ class ShardedEmbedding:
             c += lay.dims[t]
         self.dp_width = c
         self.states = [self._make_state(r, init) for r in comm.ranks]
+        # column of each shard inside its rank's full pooled row (all groups)
+        for v in range(self.W):
+            goff = np.concatenate(([0], np.cumsum(self.gwidth[v])))
+            for s_ in lay.owned[v]:
+                s_.chunk_col = int(goff[s_.grp]) + s_.out_col
+        if transport not in ("nccl", "nvlink"):
+            raise LayoutMismatch("transport must be 'nccl' or 'nvlink'")
+        if transport == "nvlink" and not isinstance(comm, NcclComm):
+            raise LayoutMismatch("the nvlink transport needs one process per GPU (NcclComm)")
+        self.transport = transport
+        if transport == "nvlink":
+            self._init_symmetric()
 
     # -- construction ----------------------------------------------------
     def _make_state(self, r: int, init) -> RankState:
@@ -243,6 +255,129 @@ class ShardedEmbedding:
             b = torch.empty(max(int(numel), 1), dtype=dtype, device=self.device)
             st.bufs[name] = b
         return b
+
+    # -- NVLink transport (symmetric memory) ------------------------------
+    def _init_symmetric(self) -> None:
+        """Receive buffers every rank can store into over NVLink: pooled rows
+        (B x sum_w width_w, source-major chunks) and upstream gradients
+        (n x max width, source-major row blocks)."""
+        import torch.distributed._symmetric_memory as symm
+
+        W, B, n = self.W, self.B, self.n
+        me = self.comm.ranks[0]
+        group = self.comm.group if self.comm.group is not None else self.comm.dist.group.WORLD
+        ef, eb = _dtype_bytes(self.fwd_comm), _dtype_bytes(self.bwd_comm)
+        self._pool_elems = B * sum(self.widths)
+        self._grad_elems = n * max(self.widths)
+        self.sym_pool = symm.empty(max(self._pool_elems, 1), dtype=self.fwd_comm, device=self.device)
+        self.sym_grad = symm.empty(max(self._grad_elems, 1), dtype=self.bwd_comm, device=self.device)
+        self.hdl_pool = symm.rendezvous(self.sym_pool, group)
+        self.hdl_grad = symm.rendezvous(self.sym_grad, group)
+        src_off = np.concatenate(([0], np.cumsum([B * wd for wd in self.widths])))
+        self.src_off = src_off
+        ptrs = self.hdl_pool.buffer_ptrs
+        # where my pooled rows land in every destination: my chunk of its receive buffer
+        self.pool_dst = torch.tensor([ptrs[v] + int(src_off[me]) * ef for v in range(W)], dtype=torch.int64,
+                                     device=self.device)
+        self.group_col = np.concatenate(([0], np.cumsum(self.gwidth[me])))
+        # remote gradient views: rows [me*B, (me+1)*B) of each owner's receive buffer
+        self.grad_peer = [self.hdl_grad.get_buffer(v, (B, max(self.widths[v], 1)), self.bwd_comm,
+                                                   me * B * max(self.widths[v], 1)) for v in range(W)]
+
+    def _step_nvlink(self, st: RankState, lr: float, eps: float, upstream_fn, ev) -> torch.Tensor:
+        lay, W, B, n = self.lay, self.W, self.B, self.n
+        me = st.rank
+        sc = st.sc
+        ev.start("fwd")
+        self._prepare_forward(st)
+        ef = _dtype_bytes(self.fwd_comm)
+        for g, grp in enumerate(st.groups):
+            if grp is None:
+                continue
+            k0, _ = self.gbounds[me][g]
+            ptrs = self.pool_dst + int(self.group_col[g]) * ef
+            grp.forward_scatter(sc["perm_ids"], sc["perm_off"][k0 * n:], n, ptrs, B, self.widths[me],
+                                self.fwd_comm)
+        self.hdl_pool.barrier(channel=0)  # every rank's rows have landed in every receive buffer
+        ev.stop("fwd")
+        pooled = self._assemble_sym(st)
+        g = upstream_fn(pooled) if upstream_fn is not None else self._ones_like(st, pooled)
+        ev.start("bwd")
+        self._pack_grad_sym(st, g)
+        self.hdl_grad.barrier(channel=1)  # all upstream blocks have landed
+        wd = self.widths[me]
+        recv = self.sym_grad[:n * wd].view(n, wd) if wd else None
+        for gi, grp in enumerate(st.groups):
+            if grp is None:
+                continue
+            k0, k1 = self.gbounds[me][gi]
+            c0, c1 = int(self.group_col[gi]), int(self.group_col[gi + 1])
+            grp.backward(sc["perm_ids"], sc["perm_off"][k0 * n:], n, recv[:, c0:c1], mode="update",
+                         optim=self.optim, lr=lr, eps=eps, table_counts=sc["shard_counts"][k0:k1])
+        self._backward_dp(st)
+        ev.stop("bwd")
+        return pooled
+
+    def _ones_like(self, st: RankState, p: torch.Tensor) -> torch.Tensor:
+        g = self._buf(st, "ones", p.numel(), p.dtype)[:p.numel()].view_as(p)
+        if st.cache.get("ones_ready") != g.data_ptr():
+            g.fill_(1.0)
+            st.cache["ones_ready"] = g.data_ptr()
+        return g
+
+    def _assemble_sym(self, st: RankState) -> torch.Tensor:
+        lay, W, B = self.lay, self.W, self.B
+        sc = st.sc
+        pooled = self._buf(st, "pooled", B * lay.total_dim, self.acc)[:B * lay.total_dim].view(B, lay.total_dim)
+        key = ("asm_sym", pooled.data_ptr(), sc["dp_out"].data_ptr() if "dp_out" in sc else 0)
+        packed = st.cache.get(key)
+        if packed is None:
+            views = {w: self.sym_pool[int(self.src_off[w]):int(self.src_off[w + 1])].view(B, self.widths[w])
+                     for w in range(W) if self.widths[w]}
+            where = {(s.table, s.index): (w, s) for w in range(W) for s in lay.owned[w]}
+            pieces, dp_pieces = [], []
+            for t in range(self.T):
+                if t in self.dp_cols:
+                    dp_pieces.append(tbe.Piece(sc["dp_out"], pooled, self.dp_cols[t], lay.model_cols[t], lay.dims[t]))
+                    continue
+                for k, i in enumerate(sorted(i for (tt, i) in where if tt == t)):
+                    w, s = where[(t, i)]
+                    pieces.append(tbe.Piece(views[w], pooled, s.chunk_col, lay.model_cols[t] + s.cols[0], s.dim,
+                                            s.kind == "row_wise" and k > 0))
+            packed = [(pl, tbe.pack_pieces(pl, self.device) if pl else None) for pl in (pieces, dp_pieces)]
+            st.cache[key] = packed
+        for pl, dev_tab in packed:
+            if pl:
+                tbe.copy_pieces(B, pl, dev_tab)
+        return pooled
+
+    def _pack_grad_sym(self, st: RankState, grad: torch.Tensor) -> None:
+        """Upstream columns of every owner's shards stored straight into the
+        owner's receive buffer (peer stores over NVLink)."""
+        lay, W, B = self.lay, self.W, self.B
+        sc = st.sc
+        grad = grad.contiguous()
+        g_dp = None
+        if st.dp_group is not None:
+            g_dp = self._buf(st, "dp_grad", B * self.dp_width, self.acc)[:B * self.dp_width].view(B, self.dp_width)
+            sc["dp_grad"] = g_dp
+        key = ("grad_sym", grad.data_ptr(), 0 if g_dp is None else g_dp.data_ptr())
+        packed = st.cache.get(key)
+        if packed is None:
+            pieces = []
+            for v in range(W):
+                for s in lay.owned[v]:
+                    pieces.append(tbe.Piece(grad, self.grad_peer[v], lay.model_cols[s.table] + s.cols[0],
+                                            s.chunk_col, s.dim))
+            dp_pieces = [tbe.Piece(grad, g_dp, lay.model_cols[t], self.dp_cols[t], lay.dims[t])
+                         for t in lay.dp_tables] if g_dp is not None else []
+            packed = [(pl, tbe.pack_pieces(pl, self.device) if pl else None) for pl in (pieces, dp_pieces)]
+            if len(st.cache) > 64:
+                st.cache.clear()
+            st.cache[key] = packed
+        for pl, dev_tab in packed:
+            if pl:
+                tbe.copy_pieces(B, pl, dev_tab)
 
     # -- byte contract ---------------------------------------------------
     def pooled_send_bytes(self, rank: int, elem_bytes: Optional[int] = None) -> int:
@@ -296,6 +431,13 @@ class ShardedEmbedding:
         S = self.states
         ev = _Timers(timers)
         self._exchange_inputs(batches)
+        if self.transport == "nvlink":
+            pooled = [self._step_nvlink(S[0], lr, eps, upstream_fn, ev)]
+            if self.lay.dp_tables:
+                self.comm.all_reduce_sum([st.dp_dense for st in S])
+                for st in S:
+                    self._dp_update(st, lr, eps)
+            return pooled
         ev.start("fwd")
         for st in S:
             self._prepare_forward(st)

@@ -168,11 +168,24 @@ class TableGroup:
         capi.check(rc, "neo_tbe_forward")
         return out
 
+    def forward_scatter(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, out_ptrs: torch.Tensor,
+                        rows_per_dst: int, out_stride: int, out_dtype: torch.dtype, pooling: str = "sum",
+                        err: Optional[ErrorRecord] = None) -> None:
+        """Forward whose pooled row b is stored at out_ptrs[b // rows_per_dst]
+        (row b % rows_per_dst, columns dim_offsets[t]..): with peer pointers
+        this performs the pooled all-to-all inside the TBE epilogue."""
+        rc = capi.lib().neo_tbe_forward_scatter(
+            self.T, batch, self.row_offsets.data_ptr(), self.dim_offsets.data_ptr(), self.max_dim,
+            self.weight_ptrs.data_ptr(), DTYPE_CODE[self.dtype], indices.data_ptr(), INDEX_CODE[indices.dtype],
+            offsets.data_ptr(), POOL_CODE[pooling], out_ptrs.data_ptr(), rows_per_dst, DTYPE_CODE[out_dtype],
+            out_stride, err.ptr if err else None, _stream())
+        capi.check(rc, "neo_tbe_forward_scatter")
+
     def backward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, grad: torch.Tensor,
                  mode: str = "update", optim: Optional[str] = None, lr: float = 0.0,
                  eps: float = 0.0, pooling: str = "sum", err: Optional[ErrorRecord] = None,
                  dense_grads: Optional[Sequence[torch.Tensor]] = None,
-                 table_counts: Optional[Sequence[int]] = None):
+                 table_counts: Optional[Sequence[int]] = None, timers: Optional[dict] = None):
         """mode "update": fused aggregate + one optimizer step per touched row
         (in place); "aggregate": returns (ids, grads, count) with global row
         keys; "dense": accumulates into dense_grads (per table, pre-zeroed).
@@ -206,7 +219,12 @@ class TableGroup:
             # rows of the whole group need > SORT_BITS key bits: run sub-groups whose
             # rows fit, so each radix sort needs one pass fewer (same results: the
             # groups' row sets are disjoint and each row is still updated once)
-            for (t0, t1) in self._sort_groups():
+            groups = self._sort_groups()
+            if self._streamed(batch, stride, pooling) and len(groups) > 1:
+                self._backward_pipelined(groups, indices, offsets, batch, grad, stride, mode_code, optim, lr,
+                                         eps, pooling, err, table_counts, timers)
+                return None
+            for (t0, t1) in groups:
                 self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling,
                                     err, t0, t1, table_counts)
             return None
@@ -234,9 +252,60 @@ class TableGroup:
                 self._group_meta[(g0, g1)] = ro
         return groups
 
+    def _streamed(self, batch: int, stride: int, pooling: str) -> bool:
+        """Mirror of the C side's streamed-path condition (f32/f16 tables,
+        rows of <= 32 vectors, SUM, 32-bit upstream offsets)."""
+        vec = 16 // torch.empty(0, dtype=self.dtype).element_size()
+        return (self.dtype != torch.float64 and pooling == "sum" and self.max_dim <= 32 * vec
+                and batch * stride < (1 << 32))
+
+    def _backward_pipelined(self, groups, indices, offsets, batch, grad, stride, mode_code, optim, lr, eps,
+                            pooling, err, table_counts, timers):
+        """PREPARE (keys + sort) of sub-group g+1 on a side stream overlaps
+        APPLY (segment walk + optimizer) of sub-group g on the caller's
+        stream; two workspaces alternate."""
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(device=self.device)
+            self._free = [torch.cuda.Event(), torch.cuda.Event()]
+        side = self._side
+        nmax = max(int(sum(table_counts[t0:t1])) for t0, t1 in groups)
+        rmax = max(int(self.row_offsets_h[t1] - self.row_offsets_h[t0]) for t0, t1 in groups)
+        wsb = capi.lib().neo_tbe_backward_workspace_bytes(nmax, rmax, self.max_dim)
+        wss = [WORKSPACE.get("tbe_bwd_a", wsb, self.device), WORKSPACE.get("tbe_bwd_b", wsb, self.device)]
+        for e in self._free:
+            e.record(main)
+        side.wait_stream(main)  # ids, offsets and weights are ready
+        prepared = []
+
+        def prepare(i):
+            t0, t1 = groups[i]
+            with torch.cuda.stream(side):
+                side.wait_event(self._free[i % 2])
+                self._backward_call(indices, offsets, batch, grad, stride, mode_code | capi.NEO_BWD_FLAG_PREPARE,
+                                    optim, lr, eps, pooling, err, t0, t1, table_counts, ws=wss[i % 2])
+                ev = torch.cuda.Event()
+                ev.record(side)
+                prepared.append(ev)
+
+        prepare(0)
+        for i, (t0, t1) in enumerate(groups):
+            if i + 1 < len(groups):
+                prepare(i + 1)
+            main.wait_event(prepared[i])
+            if timers is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(main)
+            self._backward_call(indices, offsets, batch, grad, stride, mode_code | capi.NEO_BWD_FLAG_APPLY, optim,
+                                lr, eps, pooling, err, t0, t1, table_counts, ws=wss[i % 2])
+            if timers is not None:
+                e1.record(main)
+                timers.setdefault("apply", []).append((e0, e1, t0, t1))
+            self._free[i % 2].record(main)
+
     def _backward_call(self, indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling, err,
                        t0, t1, table_counts, out_ids=None, out_grads=None, out_count=None, dense_ptrs=None,
-                       n_idx=None):
+                       n_idx=None, ws=None):
         T = t1 - t0
         if table_counts is not None:
             n_idx = int(sum(table_counts[t0:t1]))
@@ -246,8 +315,9 @@ class TableGroup:
             ro, total_rows = self.row_offsets, self.total_rows
         if n_idx == 0:
             return
-        ws_bytes = capi.lib().neo_tbe_backward_workspace_bytes(n_idx, total_rows, self.max_dim)
-        ws = WORKSPACE.get("tbe_bwd", ws_bytes, self.device)
+        if ws is None:
+            ws_bytes = capi.lib().neo_tbe_backward_workspace_bytes(n_idx, total_rows, self.max_dim)
+            ws = WORKSPACE.get("tbe_bwd", ws_bytes, self.device)
         i8, i4 = 8, 4
         rc = capi.lib().neo_tbe_backward(
             T, batch, ro.data_ptr(), total_rows, self.dim_offsets.data_ptr() + t0 * i4,

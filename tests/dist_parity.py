@@ -34,7 +34,7 @@ def main():
     plans = json.loads((ROOT / "tests" / "golden" / "steps_plans.json").read_text())
     checked = 0
     failures = []
-    for c, meta in plans.items():
+    for transport, (c, meta) in [(tr, cm) for tr in ("nccl", "nvlink") for cm in plans.items()]:
         if meta["plan"]["num_workers"] != world:
             continue
         tables = [neo.TableSpec(id=d["id"], num_rows=d["num_rows"], dim=d["dim"], avg_pooling=d["avg_pooling"],
@@ -49,7 +49,7 @@ def main():
             return torch.from_numpy(np.ascontiguousarray(full[t].values[rows[0]:rows[1], cols[0]:cols[1]]))
 
         eng = nd.ShardedEmbedding(model, plan, nd.NcclComm(), meta["local_batch"], device=dev, dtype=torch.float64,
-                                  optim=meta["kind"], init=init)
+                                  optim=meta["kind"], init=init, transport=transport)
         mine = _local_batches(batch, world)[rank]
         pooled = eng.step([mine], lr=cfg.lr, eps=cfg.eps)[0]
         outs = [torch.empty_like(pooled) for _ in range(world)]
@@ -65,13 +65,14 @@ def main():
         dist.all_gather_object(gathered, shards)
         if rank == 0:  # record, never exit early: the other ranks are in the same collectives
             if not np.array_equal(got, z[f"s{c}_sh_out"]):
-                failures.append(f"case {c}: pooled output differs (max {np.abs(got - z[f's{c}_sh_out']).max()})")
+                failures.append(f"{transport} case {c}: pooled output differs "
+                                f"(max {np.abs(got - z[f's{c}_sh_out']).max()})")
             lay = eng.lay
             for w in range(world):
                 for s in lay.owned[w]:
                     want = z[f"s{c}_sh_t{s.table}"][s.rows[0]:s.rows[1], s.cols[0]:s.cols[1]]
                     if not np.array_equal(gathered[w][f"{s.table_id}#{s.index}"], want):
-                        failures.append(f"case {c}: shard {s.table_id}#{s.index} differs")
+                        failures.append(f"{transport} case {c}: shard {s.table_id}#{s.index} differs")
         checked += 1
     ok = torch.tensor([0 if failures else 1], device=dev)
     dist.all_reduce(ok, op=dist.ReduceOp.MIN)
@@ -79,7 +80,8 @@ def main():
         for f in failures:
             print("FAIL", f, flush=True)
         if ok.item():
-            print(f"dist_parity: world {world}: {checked} golden cases bit-identical over NCCL", flush=True)
+            print(f"dist_parity: world {world}: {checked} golden cases (NCCL and NVLink transports) "
+                  "bit-identical over NCCL", flush=True)
     dist.destroy_process_group()
     sys.exit(0 if ok.item() else 1)
 
