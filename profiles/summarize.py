@@ -48,24 +48,29 @@ def kernel(path: str) -> str:
     txt = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h = rows[0]
-    ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("Metric Unit")
-    out, seen = [], set()
-    name = rows[1][ki] if len(rows) > 1 else "?"
-    out.append(f"kernel: `{name[:160]}`\n")
-    out.append("| metric | value |")
-    out.append("|---|---|")
-    for r in rows[1:]:
-        if r[mi] in KEYS and r[mi] not in seen:
-            seen.add(r[mi])
-            out.append(f"| {r[mi]} | {r[vi]} {r[ui]} |")
+    ii, ki, mi, vi, ui = (h.index("ID"), h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"),
+                          h.index("Metric Unit"))
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(io.StringIO(raw)))
-    if len(rr) > 2:
-        hdr, units, vals = rr[0], rr[1], rr[2]
-        for m in RAW:
-            if m in hdr:
-                j = hdr.index(m)
-                out.append(f"| {m} | {vals[j]} {units[j]} |")
+    out = []
+    by_id = collections.OrderedDict()
+    for r in rows[1:]:
+        by_id.setdefault(r[ii], []).append(r)
+    for n, (kid, krows) in enumerate(by_id.items()):
+        out.append(f"\n### kernel `{krows[0][ki][:150]}`\n")
+        out.append("| metric | value |")
+        out.append("|---|---|")
+        seen = set()
+        for r in krows:
+            if r[mi] in KEYS and r[mi] not in seen:
+                seen.add(r[mi])
+                out.append(f"| {r[mi]} | {r[vi]} {r[ui]} |")
+        if len(rr) > 2 + n:
+            hdr, units, vals = rr[0], rr[1], rr[2 + n]
+            for m in RAW:
+                if m in hdr:
+                    j = hdr.index(m)
+                    out.append(f"| {m} | {vals[j]} {units[j]} |")
     return "\n".join(out)
 
 
