@@ -50,7 +50,7 @@ def parse_args(argv=None):
     p.add_argument("--pooling", type=int, default=32)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--transport", choices=["nccl", "nvlink"], default="nccl",
+    p.add_argument("--transport", choices=["nccl", "nvlink"], default="nvlink",
                    help="N>1 pooled exchange: NCCL all_to_all, or stores into peers' symmetric buffers")
     p.add_argument("--no-subgroups", action="store_true",
                    help="diagnostic: one backward call over all tables (no shorter sort keys)")
@@ -456,6 +456,7 @@ def run_sharded(a, rank, world, dev):
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms, fwd_ms, bwd_ms, a2f_ms, a2b_ms = t.tolist()
     busbw = alltoall_busbw(eng, dev, world)
+    nvl = alltoall_nvlink_busbw(eng, dev, world) if a.transport == "nvlink" else None
     # per-rank algorithmic bytes of the local TBE (max over ranks of local tables)
     T_loc = max(len(eng.lay.owned[v]) for v in range(world))
     n = B * world
@@ -486,11 +487,17 @@ def run_sharded(a, rank, world, dev):
         "alltoall": {"send_bytes_per_gpu": send, "busbw_gbs": busbw["busbw_gbs"], "ms": busbw["ms"],
                      "peak_gbs": 900.0, "frac_of_nominal": busbw["busbw_gbs"] / 900.0,
                      "note": "pooled all-to-all payload of one step (per-GPU send bytes excluding self, "
-                             "comms.py:366-392) timed standalone with CUDA events, max over ranks"},
+                             "comms.py:366-392) through NCCL all_to_all_single, timed standalone with CUDA "
+                             "events, max over ranks"},
         "roofline_bwd": {"achieved": bb / (bwd_ms * 1e-3) / 1e9, "bytes_expected_U": bb, "ms": bwd_ms},
         "gpu_launches": launches_per_step * a.steps,
         "clocks": clk,
     }
+    if nvl is not None:
+        line["alltoall_nvlink"] = {**nvl, "peak_gbs": 900.0, "frac_of_nominal": nvl["busbw_gbs"] / 900.0,
+                                   "note": "the same payload stored by neo_copy_pieces straight into every "
+                                           "peer's symmetric receive buffer + a symmetric-memory barrier "
+                                           "(the transport the step uses), max over ranks"}
     if e2e is not None:
         line["e2e"] = e2e
     print(json.dumps(line), flush=True)
@@ -524,6 +531,45 @@ def alltoall_busbw(eng, dev, world) -> dict:
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
     ms = float(t.item())
     nbytes = per_peer * (world - 1) * send.element_size()
+    return {"ms": ms, "busbw_gbs": nbytes / (ms * 1e-3) / 1e9}
+
+
+def alltoall_nvlink_busbw(eng, dev, world) -> dict:
+    """Peer-store all-to-all over NVLink at the same payload: each rank's
+    (B x width) pooled block is written into every other rank's symmetric
+    buffer by one neo_copy_pieces launch, then a symmetric-memory barrier."""
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2104_05158_b200 import tbe
+
+    rank = tdist.get_rank()
+    B, wd = eng.B, max(eng.widths[rank], 1)
+    src = torch.zeros((B, wd), dtype=eng.fwd_comm, device=dev)
+    off = int(eng.src_off[rank])
+    pieces = [tbe.Piece(src, eng.hdl_pool.get_buffer(v, (B, wd), eng.fwd_comm, off), 0, 0, wd)
+              for v in range(world) if v != rank]
+    pdev = tbe.pack_pieces(pieces, dev)
+
+    def once():
+        tbe.copy_pieces(B, pieces, pdev)
+        eng.hdl_pool.barrier(channel=0)
+
+    for _ in range(3):
+        once()
+    torch.cuda.synchronize()
+    tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 10
+    e0.record()
+    for _ in range(reps):
+        once()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device=dev)
+    tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+    ms = float(t.item())
+    nbytes = B * eng.widths[rank] * (world - 1) * src.element_size()
     return {"ms": ms, "busbw_gbs": nbytes / (ms * 1e-3) / 1e9}
 
 

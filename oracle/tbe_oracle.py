@@ -295,3 +295,40 @@ def to_wtb(lengths, indices, workers: int):
     lengths = np.asarray(lengths, dtype=np.int64)
     T, n = lengths.shape
     return permute_blocks(T, workers, n // workers, lengths.reshape(-1), indices)
+
+
+# ---------------------------------------------------------------------------
+# table checkpoint format (embedding.py:334-377): b"NEOT", "<QQBB" header
+# (rows, dim, precision code FP32=0/FP16=1, moment code none=0/rowwise=1/
+# elementwise=2), then the f64 values (row-major) and the f64 moment.
+
+NEOT_MAGIC = b"NEOT"
+
+
+def neot_write(fh, values, moment=None, precision: int = 0) -> None:
+    """dump_table (embedding.py:341-360)."""
+    import struct
+
+    values = np.ascontiguousarray(values, dtype=np.float64)
+    mcode = 0 if moment is None else (1 if np.ndim(moment) == 1 else 2)
+    fh.write(NEOT_MAGIC)
+    fh.write(struct.pack("<QQBB", values.shape[0], values.shape[1], precision, mcode))
+    fh.write(values.tobytes())
+    if moment is not None:
+        fh.write(np.ascontiguousarray(moment, dtype=np.float64).tobytes())
+
+
+def neot_read(fh):
+    """load_table (embedding.py:363-377) -> (values, moment | None, precision)."""
+    import struct
+
+    if fh.read(4) != NEOT_MAGIC:
+        raise ValueError("bad table checkpoint magic")
+    rows, dim, prec, mcode = struct.unpack("<QQBB", fh.read(18))
+    values = np.frombuffer(fh.read(rows * dim * 8), dtype=np.float64).reshape(rows, dim).copy()
+    moment = None
+    if mcode == 1:
+        moment = np.frombuffer(fh.read(rows * 8), dtype=np.float64).copy()
+    elif mcode == 2:
+        moment = np.frombuffer(fh.read(rows * dim * 8), dtype=np.float64).reshape(rows, dim).copy()
+    return values, moment, prec

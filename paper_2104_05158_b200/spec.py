@@ -86,6 +86,29 @@ class TableSpec:
         return 4 if self.num_rows <= 2**31 else 8
 
 
+def model_from_json(text: str) -> "ModelSpec":
+    """ModelSpec from the reference's model document (serialize_model_spec /
+    parse_model_spec, model.py:611-683): the table list (id, num_rows, dim,
+    avg_pooling, value_precision, index_skew) and the batch/dense fields.
+    Generator-expanded table lists (model.py:544-578) are not accepted here."""
+    import json
+
+    doc = json.loads(text)
+    tabs = []
+    for i, t in enumerate(doc.get("tables", [])):
+        sk = t.get("index_skew", {"kind": "uniform"})
+        skew = IndexSkew(SkewKind(sk["kind"]), float(sk.get("alpha", 0.0)))
+        tabs.append(TableSpec(id=str(t["id"]), num_rows=int(t["num_rows"]), dim=int(t["dim"]),
+                              avg_pooling=float(t["avg_pooling"]),
+                              value_precision=Precision(t.get("value_precision", "FP32")), index_skew=skew))
+    return ModelSpec(tables=tuple(tabs), bottom_mlp_layers=tuple(tuple(x) for x in doc.get("bottom_mlp_layers", [])),
+                     top_mlp_layers=tuple(tuple(x) for x in doc.get("top_mlp_layers", [])),
+                     local_batch=int(doc.get("local_batch", 1)),
+                     mflops_per_sample=float(doc.get("mflops_per_sample", 0.0)),
+                     interaction_flops_per_sample=float(doc.get("interaction_flops_per_sample", 0.0)),
+                     dense_param_bytes=int(doc.get("dense_param_bytes", 0)))
+
+
 @dataclass(frozen=True)
 class ModelSpec:
     """Embedding tables plus the per-worker batch (model.py:100-168); the

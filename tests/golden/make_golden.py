@@ -188,15 +188,37 @@ def c1_digest() -> dict:
             "out_sum": float(out.sum()), "value_sums": [float(t.values.sum()) for t in tabs]}
 
 
-def main():
-    np.savez_compressed(OUT / "ops.npz", **op_cases())
-    z, plans = step_cases()
-    np.savez_compressed(OUT / "steps.npz", **z)
-    (OUT / "steps_plans.json").write_text(json.dumps(plans, indent=1, sort_keys=True))
-    (OUT / "c1_digest.json").write_text(json.dumps(c1_digest(), indent=1))
+def neot_cases() -> None:
+    """Table checkpoints written by the reference's dump_table
+    (embedding.py:341-360): one per moment kind, one FP16-precision spec."""
+    rng = np.random.default_rng(7)
+    d = OUT / "neot"
+    d.mkdir(exist_ok=True)
+    cases = [("rowwise", 37, 8, neosim.Precision.FP32, "rowwise"),
+             ("elementwise", 21, 5, neosim.Precision.FP32, "elementwise"),
+             ("nomoment", 16, 12, neosim.Precision.FP16, None)]
+    for name, H, D, prec, kind in cases:
+        spec = neosim.TableSpec(id=name, num_rows=H, dim=D, avg_pooling=1.0, value_precision=prec)
+        values = rng.standard_normal((H, D))
+        moment = None if kind is None else np.abs(rng.standard_normal(H if kind == "rowwise" else (H, D)))
+        with open(d / f"{name}.bin", "wb") as fh:
+            embedding.dump_table(embedding.EmbeddingTable(spec, values, moment), fh)
+
+
+def main(parts=("ops", "steps", "c1", "neot")):
+    if "ops" in parts:
+        np.savez_compressed(OUT / "ops.npz", **op_cases())
+    if "steps" in parts:
+        z, plans = step_cases()
+        np.savez_compressed(OUT / "steps.npz", **z)
+        (OUT / "steps_plans.json").write_text(json.dumps(plans, indent=1, sort_keys=True))
+    if "c1" in parts:
+        (OUT / "c1_digest.json").write_text(json.dumps(c1_digest(), indent=1))
+    if "neot" in parts:
+        neot_cases()
     for p in sorted(OUT.glob("*")):
         print(p.name, p.stat().st_size)
 
 
 if __name__ == "__main__":
-    main()
+    main(tuple(sys.argv[1:]) or ("ops", "steps", "c1", "neot"))
