@@ -50,6 +50,9 @@ def parse_args(argv=None):
     p.add_argument("--pooling", type=int, default=32)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--workload", choices=["c2", "c3", "c4", "c5"], default="c2",
+                   help="N>1 only: c2 = config 2 per GPU (weak scaling, default); c3/c4/c5 = the BASELINE "
+                        "multi-GPU configs at global batch 65,536")
     p.add_argument("--transport", choices=["nccl", "nvlink"], default="nvlink",
                    help="N>1 pooled exchange: NCCL all_to_all, or stores into peers' symmetric buffers")
     p.add_argument("--no-subgroups", action="store_true",
@@ -400,32 +403,145 @@ def expected_unique(H: int, N: int) -> float:
     return H * (1.0 - (1.0 - 1.0 / H) ** N)
 
 
+class ShardedWorkload:
+    """One BASELINE config as a sharded step: model, plan, per-rank batch,
+    wire / storage dtypes and the id distribution (device-generated)."""
+
+    def __init__(self, a, world: int):
+        import torch
+
+        from paper_2104_05158_b200 import plan as P
+        from paper_2104_05158_b200 import spec
+
+        self.key = a.workload
+        self.fwd_comm = self.bwd_comm = None
+        self.dtype = torch.float32
+        self.zipf = False
+        L = a.pooling
+        if a.workload == "c2":
+            T, H, D, self.B = a.tables, a.rows, a.dim, a.batch
+            plan_name, self.scaling = f"c2_w{world}", "weak"
+            self.name = workload_name(a)
+        elif a.workload == "c3":
+            T, H, D, self.B = 256, 2_000_000, 128, 65536 // world
+            plan_name, self.scaling = f"c3_w{world}", "strong"
+            self.name = "c3: 256 tables x 2,000,000 rows x dim 128 fp32, global batch 65,536, pooling 32"
+        elif a.workload == "c4":
+            T, H, D, self.B = 4, 100_000_000, 256, 65536 // world
+            plan_name, self.scaling = f"c4_rw_w{world}", "strong"
+            if world <= 2:
+                self.dtype = torch.float16  # 205.6 GB/GPU in fp32 (SURVEY.md 8d)
+            self.name = (f"c4: 4 tables x 100,000,000 rows x dim 256 "
+                         f"{'fp16' if world <= 2 else 'fp32'}, row-wise over {world} GPUs, global batch 65,536, "
+                         "pooling 32")
+        elif a.workload == "c5":
+            self.B = 65536 // world
+            plan_name, self.scaling = f"c5_w{world}", "strong"
+            self.fwd_comm, self.bwd_comm = torch.float16, torch.bfloat16
+            self.zipf = True
+            self.name = ("c5: 512 tables (rows log-uniform 1e3..1e7, dims 32..256, pooling 1..64, Zipf 1.05), "
+                         "mixed TW/RW/CW/DP plan, fp16 fwd / bf16 bwd all-to-all, global batch 65,536")
+        else:
+            raise SystemExit(f"unknown workload {a.workload}")
+        if a.workload == "c5":
+            self.model = spec.model_from_json((ROOT / "configs" / "models" / "c5.json").read_text())
+        else:
+            self.model = spec.ModelSpec(tables=tuple(spec.TableSpec(f"t{i}", H, D, float(L)) for i in range(T)),
+                                        local_batch=self.B)
+        self.plan_file = ROOT / "configs" / "plans" / f"{plan_name}.json"
+        self.plan = P.plan_from_json(self.plan_file.read_text())
+        self.rows = np.array([t.num_rows for t in self.model.tables], dtype=np.int64)
+        self.pool = np.array([t.avg_pooling for t in self.model.tables])
+
+    def table_bytes_per_rank(self, world: int) -> float:
+        """Largest per-rank table + moment footprint under the plan."""
+        import torch
+
+        e = torch.empty(0, dtype=self.dtype).element_size()
+        from paper_2104_05158_b200 import plan as P
+
+        lay = P.rank_layout(self.model, self.plan)
+        dp = sum(self.model.tables[t].num_rows * (self.model.tables[t].dim * e + 4) for t in lay.dp_tables)
+        return dp + max(sum(s.num_rows * (s.dim * e + 4) for s in lay.owned[v]) for v in range(world))
+
+    def lengths(self, seed: int) -> np.ndarray:
+        """(T, B) bag lengths: floor(L) + Bernoulli(frac L) (model.py:396-401)."""
+        rng = np.random.default_rng(seed)
+        base = np.floor(self.pool).astype(np.int64)[:, None]
+        frac = (self.pool - np.floor(self.pool))[:, None]
+        return base + (rng.random((len(self.pool), self.B)) < frac)
+
+    def ids(self, lengths: np.ndarray, gen, device, host: bool = False):
+        """Table-major int32 ids: uniform, or a continuous Zipf(alpha) inverse
+        CDF (bounded power law, floor) for the skewed config."""
+        import torch
+
+        counts = torch.from_numpy(lengths.sum(axis=1))
+        dev = "cpu" if host else device
+        H = torch.repeat_interleave(torch.from_numpy(self.rows), counts).to(dev)
+        u = torch.rand(H.numel(), generator=gen, device=dev, dtype=torch.float64)
+        if self.zipf:
+            alpha = 1.05
+            top = H.double().pow(1.0 - alpha)
+            x = (1.0 + u * (top - 1.0)).pow(1.0 / (1.0 - alpha))
+            ids = torch.minimum(x.floor().long() - 1, H - 1).clamp_(min=0)
+        else:
+            ids = torch.minimum((u * H).long(), H - 1)
+        return ids.to(torch.int32)
+
+
+def local_fwd_bytes(eng, wl, n, B) -> float:
+    """Compulsory forward bytes of this rank's local shards for the last
+    step's routed id counts (rows + ids + offsets + pooled write)."""
+    import torch
+
+    st = eng.states[0]
+    e = torch.empty(0, dtype=eng.dtype).element_size()
+    total = 0.0
+    shards = eng.lay.owned[st.rank]
+    for s, c in zip(shards, st.sc.get("shard_counts", [])):
+        total += c * (s.dim * e + 4) + (n + 1) * 8 + n * s.dim * 4
+    for t, c in zip(eng.lay.dp_tables, st.sc.get("dp_counts", [])):
+        D = wl.model.tables[t].dim
+        total += c * (D * e + 4) + (B + 1) * 8 + B * D * 4
+    return total
+
+
 def run_sharded(a, rank, world, dev):
-    """N>1: sharded embedding step over NCCL, weak scaling (B per GPU fixed)."""
+    """N>1: sharded embedding step (one rank per GPU).  c2 (default): the
+    single-GPU config's per-GPU work at every N (weak scaling); c3/c4/c5:
+    the BASELINE multi-GPU configs at a fixed global batch (strong)."""
     import torch
     import torch.distributed as tdist
 
     from paper_2104_05158_b200 import dist as nd
-    from paper_2104_05158_b200 import plan as P
-    from paper_2104_05158_b200 import spec
 
     tdist.init_process_group("nccl", device_id=dev)
-    T, H, D, B, L = a.tables, a.rows, a.dim, a.batch, a.pooling
-    plan_file = ROOT / "configs" / "plans" / f"c2_w{world}.json"
-    plan = P.plan_from_json(plan_file.read_text())
-    model = spec.ModelSpec(tables=tuple(spec.TableSpec(f"t{i}", H, D, float(L)) for i in range(T)), local_batch=B)
+    wl = ShardedWorkload(a, world)
+    B = wl.B
+    need = wl.table_bytes_per_rank(world)
+    have = torch.cuda.get_device_properties(dev).total_memory
+    if need > 0.75 * have:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "unavailable": f"{a.workload} at {world} GPUs needs "
+                              f"{need / 1e9:.0f} GB of tables per GPU (> 75% of {have / 1e9:.0f} GB); "
+                              "run it on more GPUs"}), flush=True)
+        tdist.destroy_process_group()
+        return
     comm = nd.NcclComm()
-    eng = nd.ShardedEmbedding(model, plan, comm, B, device=dev, dtype=torch.float32, optim="rowwise_adagrad",
-                              index_dtype=torch.int32, transport=a.transport)
+    eng = nd.ShardedEmbedding(wl.model, wl.plan, comm, B, device=dev, dtype=wl.dtype, optim="rowwise_adagrad",
+                              index_dtype=torch.int32, transport=a.transport, fwd_comm=wl.fwd_comm,
+                              bwd_comm=wl.bwd_comm)
     torch.manual_seed(rank)
     for st in eng.states:
-        for grp in st.groups:
+        for grp in list(st.groups) + [st.dp_group]:
             if grp is not None:
-                grp._storage.normal_()
-    lengths = np.full((T, B), L, dtype=np.int64)
-    L_dev = torch.full((T * B,), L, dtype=torch.int64, device=dev)
+                for w in grp.weights:
+                    w.normal_()
+    lengths = wl.lengths(77 + rank)
+    L_dev = torch.from_numpy(lengths.reshape(-1)).to(dev)
     g = torch.Generator(device=dev).manual_seed(1234 + rank)
-    ids = [torch.randint(0, H, (T * B * L,), dtype=torch.int32, device=dev, generator=g) for _ in range(2)]
+    ids = [wl.ids(lengths, g, dev) for _ in range(2)]
 
     def step(i, timers=None):
         return eng.step([(lengths, ids[i % 2], L_dev)], lr=LR, eps=EPS, timers=timers)
@@ -451,37 +567,40 @@ def run_sharded(a, rank, world, dev):
     clk = clocks.stop() if clocks else None
     ms_local = e0.elapsed_time(e1) / a.steps
     ph = {k: float(np.mean([x.elapsed_time(y) for x, y in v])) for k, v in timers.items()}
+    n = B * world
+    fb_local = local_fwd_bytes(eng, wl, n, B)
+    fwd_gbs_local = fb_local / (ph.get("fwd", 1.0) * 1e-3) / 1e9
     t = torch.tensor([ms_local, ph.get("fwd", 0.0), ph.get("bwd", 0.0), ph.get("a2a_fwd", 0.0),
-                      ph.get("a2a_bwd", 0.0)], dtype=torch.float64, device=dev)
+                      ph.get("a2a_bwd", 0.0), fb_local], dtype=torch.float64, device=dev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms, fwd_ms, bwd_ms, a2f_ms, a2b_ms = t.tolist()
+    ms, fwd_ms, bwd_ms, a2f_ms, a2b_ms, fb_max = t.tolist()
+    tmin = torch.tensor([fwd_gbs_local], dtype=torch.float64, device=dev)
+    tdist.all_reduce(tmin, op=tdist.ReduceOp.MIN)
     busbw = alltoall_busbw(eng, dev, world)
     nvl = alltoall_nvlink_busbw(eng, dev, world) if a.transport == "nvlink" else None
-    # per-rank algorithmic bytes of the local TBE (max over ranks of local tables)
-    T_loc = max(len(eng.lay.owned[v]) for v in range(world))
-    n = B * world
-    N = n * L
-    U = expected_unique(H, N)
-    fb = fwd_bytes(T_loc, N, D, n)
-    bb = bwd_bytes([U] * T_loc, N, D, n)
     peak, peak_kind = hbm_peak()
     send = max(eng.pooled_send_bytes(v) for v in range(world))
-    e2e = None if a.no_e2e else e2e_sharded(a, eng, rank, world, dev, lengths, L_dev)
+    e2e = None if a.no_e2e else e2e_sharded(a, wl, eng, rank, world, dev, lengths, L_dev)
     if rank != 0:
         tdist.destroy_process_group()
         return
-    fwd_gbs = fb / (fwd_ms * 1e-3) / 1e9
+    fwd_gbs = fb_max / (fwd_ms * 1e-3) / 1e9
+    kinds = sorted({x.scheme.kind.value for x in wl.plan.assignments})
     line = {
-        "metric": METRIC, "value": B * world / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
-        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": workload_name(a) + f", sharded over {world} GPUs ({plan_file.name}: reference "
-                   "plan_4d, table-wise)", "tables": T, "rows": H, "dim": D, "batch_per_gpu": B,
-                   "global_batch": B * world, "pooling": L, "parallelism": f"tw{world}",
+        "metric": METRIC, "value": n / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": wl.scaling,
+        "vs_baseline": None, "dtype": "f16" if wl.dtype == torch.float16 else "f32", "data": "synthetic",
+        "config": {"workload": wl.name + f", sharded over {world} GPUs ({wl.plan_file.name})",
+                   "tables": wl.model.num_tables, "batch_per_gpu": B, "global_batch": n,
+                   "lookups_per_step": int(lengths.sum()) * world, "schemes": kinds,
+                   "parallelism": "+".join({"table_wise": "tw", "row_wise": "rw", "column_wise": "cw",
+                                            "data_parallel": "dp"}[k] for k in kinds) + str(world),
+                   "wire": {"fwd": str(eng.fwd_comm).replace("torch.", ""),
+                            "bwd": str(eng.bwd_comm).replace("torch.", "")},
                    "l2": "inputs larger than L2"},
-        "roofline": {"bound": "hbm", "kernel": "tbe_forward_kernel (local shards)", "achieved": fwd_gbs, "peak": peak,
-                     "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak, "traffic": None,
-                     "algorithmic_bytes": fb, "ms": fwd_ms},
+        "roofline": {"bound": "hbm", "kernel": "tbe_forward_kernel (local shards; slowest rank)", "achieved": fwd_gbs,
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak, "traffic": None,
+                     "algorithmic_bytes": fb_max, "ms": fwd_ms, "min_rank_gbs": float(tmin.item())},
         "phases_ms": {"fwd_incl_overlapped_a2a": fwd_ms, "a2a_fwd_tail": a2f_ms,
                       "bwd_incl_overlapped_a2a": bwd_ms, "overlap_groups": eng.G, "transport": a.transport},
         "alltoall": {"send_bytes_per_gpu": send, "busbw_gbs": busbw["busbw_gbs"], "ms": busbw["ms"],
@@ -489,10 +608,14 @@ def run_sharded(a, rank, world, dev):
                      "note": "pooled all-to-all payload of one step (per-GPU send bytes excluding self, "
                              "comms.py:366-392) through NCCL all_to_all_single, timed standalone with CUDA "
                              "events, max over ranks"},
-        "roofline_bwd": {"achieved": bb / (bwd_ms * 1e-3) / 1e9, "bytes_expected_U": bb, "ms": bwd_ms},
         "gpu_launches": launches_per_step * a.steps,
         "clocks": clk,
     }
+    if a.workload == "c2":
+        U = expected_unique(a.rows, n * a.pooling)
+        T_loc = max(len(eng.lay.owned[v]) for v in range(world))
+        bb = bwd_bytes([U] * T_loc, n * a.pooling, a.dim, n)
+        line["roofline_bwd"] = {"achieved": bb / (bwd_ms * 1e-3) / 1e9, "bytes_expected_U": bb, "ms": bwd_ms}
     if nvl is not None:
         line["alltoall_nvlink"] = {**nvl, "peak_gbs": 900.0, "frac_of_nominal": nvl["busbw_gbs"] / 900.0,
                                    "note": "the same payload stored by neo_copy_pieces straight into every "
@@ -573,16 +696,16 @@ def alltoall_nvlink_busbw(eng, dev, world) -> dict:
     return {"ms": ms, "busbw_gbs": nbytes / (ms * 1e-3) / 1e9}
 
 
-def e2e_sharded(a, eng, rank, world, dev, lengths, L_dev) -> dict:
+def e2e_sharded(a, wl, eng, rank, world, dev, lengths, L_dev) -> dict:
     """Sharded step with host (pinned) ids copied H2D each step on a side
     stream (prefetch of the next batch overlaps the current step) and the
     loss read back D2H."""
     import torch
     import torch.distributed as tdist
 
-    T, H, B, L = a.tables, a.rows, a.batch, a.pooling
+    B = wl.B
     gen = torch.Generator().manual_seed(99 + rank)
-    host = [torch.randint(0, H, (T * B * L,), dtype=torch.int32, generator=gen).pin_memory() for _ in range(2)]
+    host = [wl.ids(lengths, gen, dev, host=True).pin_memory() for _ in range(2)]
     dev_ids = [torch.empty_like(h, device=dev) for h in host]
     copied = [torch.cuda.Event() for _ in range(2)]
     free = [torch.cuda.Event() for _ in range(2)]

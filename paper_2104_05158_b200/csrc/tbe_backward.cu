@@ -718,6 +718,7 @@ tbe_stream_update_kernel(SegParams p) {
   }
 }
 
+// ---------------------------------------------------------------------------
 template <typename W, typename G, typename Key, int OPT>
 static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
   const bool full_rows = (p.flags & NEO_BWD_FLAG_FULL_ROWS) != 0;
