@@ -145,21 +145,30 @@ copy_pieces_kernel(int64_t rows, const neo_piece* __restrict__ pieces, int32_t n
     const neo_piece pc = pieces[pi];
     const S* src = reinterpret_cast<const S*>(pc.src) + r * pc.src_stride + pc.src_col;
     D* dst = reinterpret_cast<D*>(pc.dst) + r * pc.dst_stride + pc.dst_col;
-    constexpr int V = 4;
-    const bool vec = sizeof(S) == 4 && sizeof(D) == 4 && (pc.width % V) == 0 &&
-                     (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
+    // 16-byte accesses on the narrower side (8 x 16-bit or 4 x 32-bit
+    // elements per lane); f64 pieces take the scalar path
+    constexpr int kMin = sizeof(S) < sizeof(D) ? sizeof(S) : sizeof(D);
+    constexpr int V = 16 / kMin;
+    constexpr bool kVecOk = sizeof(S) <= 4 && sizeof(D) <= 4;
+    const bool vec = kVecOk && (pc.width % V) == 0 && (reinterpret_cast<uintptr_t>(src) % 16) == 0 &&
                      (reinterpret_cast<uintptr_t>(dst) % 16) == 0;
     if (vec) {
       for (int j = lane * V; j < pc.width; j += kWarp * V) {
         Vec<S, V> a = ld_vec<S, V>(src + j);
         Vec<D, V> o;
-        if (pc.accumulate) o = *reinterpret_cast<const Vec<D, V>*>(dst + j);
+        if (pc.accumulate) {  // coherent 16-byte loads: earlier pieces of this launch wrote dst
+#pragma unroll
+          for (int q = 0; q < (int)(sizeof(D) * V) / 16; ++q)
+            reinterpret_cast<uint4*>(&o)[q] = reinterpret_cast<const uint4*>(dst + j)[q];
+        }
 #pragma unroll
         for (int e = 0; e < V; ++e) {
           const float x = Elem<S>::to_f(a.v[e]);
           o.v[e] = pc.accumulate ? Elem<D>::from_f(Elem<D>::to_f(o.v[e]) + x) : Elem<D>::from_f(x);
         }
-        st_vec<D, V>(dst + j, o);
+#pragma unroll
+        for (int q = 0; q < (int)(sizeof(D) * V) / 16; ++q)
+          reinterpret_cast<uint4*>(dst + j)[q] = reinterpret_cast<const uint4*>(&o)[q];
       }
     } else {
       for (int j = lane; j < pc.width; j += kWarp) {

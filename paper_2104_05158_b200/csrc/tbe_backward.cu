@@ -307,12 +307,12 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 
-template <typename W, typename G>
+template <typename W, typename G, int VPL>
 struct alignas(16) StreamSmem {
   static constexpr int kVec = 16 / sizeof(W);
-  static constexpr int kGBytes = kVec * sizeof(G);  // upstream bytes per lane per row
-  unsigned char g[kGRing][kWarp][kGBytes];
-  unsigned char w[kWRing][kWarp][16];
+  static constexpr int kGBytes = kVec * sizeof(G);  // upstream bytes per lane per row vector
+  unsigned char g[kGRing][kWarp][kGBytes * VPL];
+  unsigned char w[kWRing][kWarp][16 * VPL];
   float mr[kWRing];               // row-wise moment
 };
 
@@ -370,13 +370,19 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
 
 constexpr int kChunk = 128;  // sorted entries owned per warp task (4 windows)
 
+// element index of (vector v of lane, element e): the vector path gives lane
+// contiguous 16-byte vectors lane, lane+32, ...; the scalar path strides by 32
+__device__ __forceinline__ int elem_index(bool vec, int lane, int v, int e, int kVec) {
+  return vec ? (lane + v * kWarp) * kVec + e : lane + (v * kVec + e) * kWarp;
+}
+
 // Hot rows (skewed ids): a 128-entry chunk whose entries all belong to ONE
 // row (no segment boundary inside, and it does not start the row) gets its
 // upstream partial sum precomputed here, in entry order, by its own warp.
 // The streamed kernel then folds such partials into the row's gradient in
 // chunk order instead of walking the row's occurrences on a single warp, so
 // a row touched 1e5 times costs ~1e3 partial loads, not 1e5 serial gathers.
-template <typename W, typename G, typename Key>
+template <typename W, typename G, typename Key, int VPL>
 __global__ void __launch_bounds__(256)
 hot_chunk_kernel(SegParams p) {
   constexpr int kVec = 16 / sizeof(W);
@@ -406,48 +412,53 @@ hot_chunk_kernel(SegParams p) {
       const bool vec = (D % kVec) == 0 && aligned16(reinterpret_cast<const void*>(p.weights[t])) &&
                        (doff % kVec) == 0 && (p.grad_stride % kVec) == 0 &&
                        (reinterpret_cast<uintptr_t>(grad) % min(16, (int)(sizeof(G) * kVec))) == 0;
-      float acc[kVec];
+      float acc[VPL][kVec];
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
-      const int32_t mybag = p.bags[c0 + lane];
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) acc[v][e] = 0.f;
       for (int q = 0; q < kChunk; q += kWarp) {
         const int32_t qb = p.bags[c0 + q + lane];
-#pragma unroll 8
+#pragma unroll 4
         for (int e2 = 0; e2 < kWarp; ++e2) {
           const int32_t bag = __shfl_sync(full, qb, e2);
           const G* src = grad + ((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + doff;
-          if (vec) {
-            if (lane * kVec < D) {
-              Vec<G, kVec> v = ld_vec<G, kVec>(src + lane * kVec);
 #pragma unroll
-              for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(v.v[e]);
-            }
-          } else {
+          for (int v = 0; v < VPL; ++v) {
+            if (vec) {
+              if ((lane + v * kWarp) * kVec < D) {
+                Vec<G, kVec> x = ld_vec<G, kVec>(src + (lane + v * kWarp) * kVec);
 #pragma unroll
-            for (int e = 0; e < kVec; ++e) {
-              const int j = lane + e * kWarp;
-              if (j < D) acc[e] += Elem<G>::to_f(src[j]);
+                for (int e = 0; e < kVec; ++e) acc[v][e] += Elem<G>::to_f(x.v[e]);
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < kVec; ++e) {
+                const int j = lane + (v * kVec + e) * kWarp;
+                if (j < D) acc[v][e] += Elem<G>::to_f(src[j]);
+              }
             }
           }
         }
       }
-      (void)mybag;
       float* dst = p.pool + (int64_t)slot * p.max_dim;
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) {
-        const int j = vec ? lane * kVec + e : lane + e * kWarp;
-        if (j < D) dst[j] = acc[e];
-      }
+      for (int v = 0; v < VPL; ++v)
+#pragma unroll
+        for (int e = 0; e < kVec; ++e) {
+          const int j = elem_index(vec, lane, v, e, kVec);
+          if (j < D) dst[j] = acc[v][e];
+        }
     }
     if (lane == 0) p.chunk_slot[c] = slot;
   }
 }
 
 
-template <typename W, typename G, typename Key, int OPT, bool FULL>
-__global__ void __launch_bounds__(kStreamWarps * kWarp, 6)
+template <typename W, typename G, typename Key, int OPT, bool FULL, int VPL>
+__global__ void __launch_bounds__(kStreamWarps * kWarp, VPL == 1 ? 6 : 3)
 tbe_stream_update_kernel(SegParams p) {
-  using SM = StreamSmem<W, G>;
+  using SM = StreamSmem<W, G, VPL>;
   constexpr int kVec = SM::kVec;
   constexpr int kGB = SM::kGBytes;
   const unsigned full = 0xffffffffu;
@@ -457,7 +468,6 @@ tbe_stream_update_kernel(SegParams p) {
   const Key* keys = reinterpret_cast<const Key*>(p.keys);
   const int64_t N = p.N;
   const int64_t nchunks = (N + kChunk - 1) / kChunk;
-  const int64_t nwarps = (int64_t)gridDim.x * kStreamWarps;
   const float lr = (float)p.lr, eps = (float)p.eps;
   const G* gbase = reinterpret_cast<const G*>(p.grad);
 #ifndef NEO_L2_HINTS
@@ -473,7 +483,6 @@ tbe_stream_update_kernel(SegParams p) {
   // static grid stride lets warps drift apart over hundreds of chunks).
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(p.chunk_counter);
   __shared__ long long s_claim[kStreamWarps];
-  (void)nwarps;
   for (;;) {
     __syncwarp();
     if (lane == 0) s_claim[warp] = (long long)atomicAdd(counter, 1ull);
@@ -534,11 +543,14 @@ tbe_stream_update_kernel(SegParams p) {
             }
             const W* wrow = reinterpret_cast<const W*>(__shfl_sync(full, pw.wptr, l));
             if (FULL || pvec) {
-              if (FULL || lane * kVec < pD) cp_async_hint(&sm.w[pslot][lane][0], wrow + lane * kVec, 16, pol_stream);
+#pragma unroll
+              for (int v = 0; v < VPL; ++v)
+                if (FULL || (lane + v * kWarp) * kVec < pD)
+                  cp_async_hint(&sm.w[pslot][lane][16 * v], wrow + (lane + v * kWarp) * kVec, 16, pol_stream);
             } else {  // unaligned table: synchronous strided staging (own lane's slice)
               W* ws = reinterpret_cast<W*>(&sm.w[pslot][lane][0]);
 #pragma unroll
-              for (int e = 0; e < kVec; ++e) {
+              for (int e = 0; e < kVec * VPL; ++e) {
                 const int j = lane + e * kWarp;
                 ws[e] = j < pD ? wrow[j] : W(0);
               }
@@ -551,18 +563,23 @@ tbe_stream_update_kernel(SegParams p) {
           const int gs = pe & (kGRing - 1);
           const G* grow = gbase + __shfl_sync(full, pw.gofs, l);
           if (FULL || pvec) {
-            if (FULL || lane * kVec < pD) {
-              if constexpr (kGB == 32) {
-                cp_async_hint(&sm.g[gs][lane][0], grow + lane * kVec, 16, pol_keep);
-                cp_async_hint(&sm.g[gs][lane][16], grow + lane * kVec + kVec / 2, 16, pol_keep);
-              } else {
-                cp_async_hint(&sm.g[gs][lane][0], grow + lane * kVec, kGB, pol_keep);
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              if (FULL || (lane + v * kWarp) * kVec < pD) {
+                const G* src = grow + (lane + v * kWarp) * kVec;
+                unsigned char* dst = &sm.g[gs][lane][kGB * v];
+                if constexpr (kGB == 32) {
+                  cp_async_hint(dst, src, 16, pol_keep);
+                  cp_async_hint(dst + 16, src + kVec / 2, 16, pol_keep);
+                } else {
+                  cp_async_hint(dst, src, kGB, pol_keep);
+                }
               }
             }
           } else {
             G* gsm = reinterpret_cast<G*>(&sm.g[gs][lane][0]);
 #pragma unroll
-            for (int e = 0; e < kVec; ++e) {
+            for (int e = 0; e < kVec * VPL; ++e) {
               const int j = lane + e * kWarp;
               gsm[e] = j < pD ? grow[j] : G(0);
             }
@@ -574,76 +591,87 @@ tbe_stream_update_kernel(SegParams p) {
     };
 
     // consumer state: current segment (registers) and its accumulator
-    float acc[kVec];
+    float acc[VPL * kVec];
 #pragma unroll
-    for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
+    for (int e = 0; e < VPL * kVec; ++e) acc[e] = 0.f;
     int cslot = -1;
     uint64_t cw_w = 0, cw_m = 0;
     int cD = 0, cvec = 0;
     float cinvD = 0.f;
     uint64_t cseg_key = 0;
-    bool lane_live = false;
+
+    auto live_at = [&](int v, int e) -> bool {  // element (v, e) of this lane is inside the row
+      if (FULL) return true;
+      return elem_index(cvec, lane, v, e, kVec) < cD;
+    };
 
     auto finalize = [&]() {  // exactly one optimizer step for the row (embedding.py:212-254)
-      if (!FULL && !lane_live) {
+      if (!FULL) {
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int e = 0; e < kVec; ++e)
+            if (!live_at(v, e)) acc[v * kVec + e] = 0.f;
       }
       bool nz = false;
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) nz |= acc[e] != 0.f;
+      for (int e = 0; e < VPL * kVec; ++e) nz |= acc[e] != 0.f;
       if (OPT == NEO_OPT_SGD || __any_sync(full, nz)) {
         const W* wsm = reinterpret_cast<const W*>(&sm.w[cslot][lane][0]);
         float scale = lr;
         if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
           float ss = 0.f;
 #pragma unroll
-          for (int e = 0; e < kVec; ++e) ss += acc[e] * acc[e];
+          for (int e = 0; e < VPL * kVec; ++e) ss += acc[e] * acc[e];
           ss = warp_sum(ss);
           const float m = __shfl_sync(full, sm.mr[cslot], 0) + ss * cinvD;
           if (lane == 0) *reinterpret_cast<float*>(cw_m) = m;
           scale = __fdividef(lr, __fsqrt_rn(m) + eps);
         }
-        W out[kVec];
-        float mo[kVec];
-#pragma unroll
-        for (int e = 0; e < kVec; ++e) {
-          const float w = Elem<W>::to_f(wsm[e]);
-          if (OPT == NEO_OPT_ADAGRAD) {  // element-wise state read here (not staged)
-            const int j = cvec ? lane * kVec + e : lane + e * kWarp;
-            const float mj = (j < cD ? reinterpret_cast<const float*>(cw_m)[j] : 0.f) + acc[e] * acc[e];
-            mo[e] = mj;
-            out[e] = Elem<W>::from_f(w - __fdividef(lr * acc[e], __fsqrt_rn(mj) + eps));
-          } else {
-            out[e] = Elem<W>::from_f(w - acc[e] * scale);
-          }
-        }
         W* wrow = reinterpret_cast<W*>(cw_w);
         float* mrow = reinterpret_cast<float*>(cw_m);
-        if (FULL || cvec) {
-          if (FULL || lane_live) {
-            Vec<W, kVec> o;
 #pragma unroll
-            for (int e = 0; e < kVec; ++e) o.v[e] = out[e];
-            st_v4_hint(wrow + lane * kVec, *reinterpret_cast<const uint4*>(&o), pol_stream);
-            if (OPT == NEO_OPT_ADAGRAD) {
-#pragma unroll
-              for (int e = 0; e < kVec; ++e) mrow[lane * kVec + e] = mo[e];
-            }
-          }
-        } else {
+        for (int v = 0; v < VPL; ++v) {
+          W out[kVec];
+          float mo[kVec];
 #pragma unroll
           for (int e = 0; e < kVec; ++e) {
-            const int j = lane + e * kWarp;
-            if (j < cD) {
-              wrow[j] = out[e];
-              if (OPT == NEO_OPT_ADAGRAD) mrow[j] = mo[e];
+            const float w = Elem<W>::to_f(wsm[v * kVec + e]);
+            const float a = acc[v * kVec + e];
+            if (OPT == NEO_OPT_ADAGRAD) {  // element-wise state read here (not staged)
+              const int j = elem_index(cvec, lane, v, e, kVec);
+              const float mj = (FULL || j < cD ? mrow[j] : 0.f) + a * a;
+              mo[e] = mj;
+              out[e] = Elem<W>::from_f(w - __fdividef(lr * a, __fsqrt_rn(mj) + eps));
+            } else {
+              out[e] = Elem<W>::from_f(w - a * scale);
+            }
+          }
+          if (FULL || cvec) {
+            if (FULL || (lane + v * kWarp) * kVec < cD) {
+              Vec<W, kVec> o;
+#pragma unroll
+              for (int e = 0; e < kVec; ++e) o.v[e] = out[e];
+              st_v4_hint(wrow + (lane + v * kWarp) * kVec, *reinterpret_cast<const uint4*>(&o), pol_stream);
+              if (OPT == NEO_OPT_ADAGRAD) {
+#pragma unroll
+                for (int e = 0; e < kVec; ++e) mrow[(lane + v * kWarp) * kVec + e] = mo[e];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < kVec; ++e) {
+              const int j = lane + (v * kVec + e) * kWarp;
+              if (j < cD) {
+                wrow[j] = out[e];
+                if (OPT == NEO_OPT_ADAGRAD) mrow[j] = mo[e];
+              }
             }
           }
         }
       }
 #pragma unroll
-      for (int e = 0; e < kVec; ++e) acc[e] = 0.f;
+      for (int e = 0; e < VPL * kVec; ++e) acc[e] = 0.f;
     };
 
 #pragma unroll 1
@@ -669,20 +697,18 @@ tbe_stream_update_kernel(SegParams p) {
           cseg_key = __shfl_sync(full, cw.key, l);
           if (OPT != NEO_OPT_SGD) cw_m = __shfl_sync(full, cw.mptr, l);
           if (FULL) {
-            cD = kWarp * kVec;
+            cD = kWarp * kVec * VPL;
             cvec = 1;
-            cinvD = 1.0f / (float)(kWarp * kVec);
-            lane_live = true;
+            cinvD = 1.0f / (float)(kWarp * kVec * VPL);
           } else {
             cD = __shfl_sync(full, cw.D, l);
             cvec = __shfl_sync(full, cw.vec, l);
             cinvD = __frcp_rn((float)cD);
-            lane_live = cvec ? lane * kVec < cD : true;
           }
         }
         const G* gsm = reinterpret_cast<const G*>(&sm.g[ce & (kGRing - 1)][lane][0]);
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
+        for (int e = 0; e < VPL * kVec; ++e) acc[e] += Elem<G>::to_f(gsm[e]);
       }
       if (stop || (pend >= 0 && ce >= pend)) break;  // range may end exactly at a window edge
       cw = pw;  // the producer is already in the next window
@@ -696,10 +722,12 @@ tbe_stream_update_kernel(SegParams p) {
         if (slot < 0) break;
         const float* src = p.pool + (int64_t)slot * p.max_dim;
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) {
-          const int j = cvec ? lane * kVec + e : lane + e * kWarp;
-          if (j < cD) acc[e] += src[j];
-        }
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            const int j = elem_index(cvec, lane, v, e, kVec);
+            if (j < cD) acc[v * kVec + e] += src[j];
+          }
       }
       for (int64_t e0 = c * kChunk; e0 < N; ++e0) {
         if ((uint64_t)keys[e0] != cseg_key) break;
@@ -707,10 +735,12 @@ tbe_stream_update_kernel(SegParams p) {
         const int32_t t = bag / (int32_t)p.B;
         const G* src = gbase + ((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + p.dim_offsets[t];
 #pragma unroll
-        for (int e = 0; e < kVec; ++e) {
-          const int j = cvec ? lane * kVec + e : lane + e * kWarp;
-          if (j < cD) acc[e] += Elem<G>::to_f(src[j]);
-        }
+        for (int v = 0; v < VPL; ++v)
+#pragma unroll
+          for (int e = 0; e < kVec; ++e) {
+            const int j = elem_index(cvec, lane, v, e, kVec);
+            if (j < cD) acc[v * kVec + e] += Elem<G>::to_f(src[j]);
+          }
       }
     }
     if (cslot >= 0) finalize();
@@ -719,12 +749,14 @@ tbe_stream_update_kernel(SegParams p) {
 }
 
 // ---------------------------------------------------------------------------
-template <typename W, typename G, typename Key, int OPT>
-static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
-  const bool full_rows = (p.flags & NEO_BWD_FLAG_FULL_ROWS) != 0;
-  auto kern = full_rows ? tbe_stream_update_kernel<W, G, Key, OPT, true>
-                        : tbe_stream_update_kernel<W, G, Key, OPT, false>;
-  const size_t smem = sizeof(StreamSmem<W, G>) * kStreamWarps;
+template <typename W, typename G, typename Key, int OPT, int VPL>
+static int launch_stream_vpl(const SegParams& p, cudaStream_t s) {
+  // guard-free instantiation when every row is exactly 32 lanes x one vector
+  auto kern = tbe_stream_update_kernel<W, G, Key, OPT, false, VPL>;
+  if constexpr (VPL == 1) {
+    if (p.flags & NEO_BWD_FLAG_FULL_ROWS) kern = tbe_stream_update_kernel<W, G, Key, OPT, true, 1>;
+  }
+  const size_t smem = sizeof(StreamSmem<W, G, VPL>) * kStreamWarps;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve shared memory");
@@ -743,12 +775,19 @@ static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
   {
     const int64_t hb = (chunks + 7) / 8;
     const unsigned hgrid = (unsigned)(hb < (int64_t)sms * 16 ? (hb > 0 ? hb : 1) : (int64_t)sms * 16);
-    hot_chunk_kernel<W, G, Key><<<hgrid, 256, 0, s>>>(p);
+    hot_chunk_kernel<W, G, Key, VPL><<<hgrid, 256, 0, s>>>(p);
     const int rc = check_launch("neo_tbe_backward(hot chunks)");
     if (rc) return rc;
   }
   kern<<<(unsigned)grid, kStreamWarps * kWarp, smem, s>>>(p);
   return check_launch("neo_tbe_backward(stream)");
+}
+
+template <typename W, typename G, typename Key, int OPT>
+static int launch_stream_opt(const SegParams& p, cudaStream_t s) {
+  // rows of up to 32 lanes x 1 or 2 sixteen-byte vectors
+  if (p.max_dim <= kWarp * (16 / (int)sizeof(W))) return launch_stream_vpl<W, G, Key, OPT, 1>(p, s);
+  return launch_stream_vpl<W, G, Key, OPT, 2>(p, s);
 }
 
 template <typename W, typename G, typename Key>
@@ -860,7 +899,7 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   const bool apply_only = (p.flags & NEO_BWD_FLAG_APPLY) != 0;
   const int wvec = weight_dtype == NEO_F16 ? 8 : 4;
   const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
-                    p.max_dim <= kWarp * wvec && !out_count &&
+                    p.max_dim <= 2 * kWarp * wvec && !out_count &&
                     p.B * p.grad_stride < (int64_t(1) << 32);  // 32-bit upstream offsets
   if ((prepare_only || apply_only) && !fast)
     return fail(NEO_E_ARG, "neo_tbe_backward: PREPARE/APPLY need the streamed UPDATE path");

@@ -194,10 +194,12 @@ def test_group_forward_f32_tolerance(pkg, wdtype, idtype):
         col += D
 
 
-# dims sets: the first has a 256-wide f32 table (general segment kernel), the
-# second fits the streamed fast path (incl. an unaligned D=100 table)
+# dims sets: the first has a 256-wide f32 table (streamed path, two vectors per
+# lane), the second an unaligned D=100 table, the fifth unaligned wide rows
+# (D=200 / 250: scalar staging with two vectors per lane)
 # (f32 D=128 / f16 D=256 tables select the guard-free FULL_ROWS kernel)
 @pytest.mark.parametrize("dims,rows", [([64, 128, 32, 256], [3000, 5000, 800, 2000]),
+                                       ([200, 8, 250], [2500, 900, 1800]),
                                        ([64, 128, 32, 8, 100], [3000, 5000, 40, 2000, 700]),
                                        ([128, 128, 128], [4000, 300, 9000]),
                                        ([256, 256], [3000, 500])])
@@ -316,7 +318,7 @@ def test_backward_subgroup_split_bitwise(pkg, monkeypatch):
     assert torch.equal(res[0][0], res[1][0]) and torch.equal(res[0][1], res[1][1])
 
 
-@pytest.mark.parametrize("dims", [[128, 128], [64, 32]])
+@pytest.mark.parametrize("dims", [[128, 128], [64, 32], [256, 64], [200, 256]])
 def test_hot_rows_skewed(pkg, dims):
     """Skewed ids (a few rows hit thousands of times): rows spanning many
     128-entry chunks are folded from precomputed chunk partials; results
