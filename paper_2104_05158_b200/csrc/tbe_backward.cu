@@ -26,6 +26,8 @@
 // pairwise order for the row mean and no FMA contraction, so results are
 // bit-identical to the reference.
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 #include <cub/device/device_radix_sort.cuh>
@@ -748,6 +750,33 @@ tbe_stream_update_kernel(SegParams p) {
   }
 }
 
+#include "tbe_pipe.cuh"
+
+// backward fast-path variant: the warp-specialised pipeline (default) or the
+// single-warp streamed walk (NEO_BWD_VARIANT=stream, kept for A/B runs)
+static bool use_pipe_variant() {
+  const char* v = std::getenv("NEO_BWD_VARIANT");
+  return !(v && std::strcmp(v, "stream") == 0);
+}
+
+template <typename W, typename G, typename Key, int OPT, int VPL>
+static int launch_pipe(const SegParams& p, cudaStream_t s, int sms) {
+  using Cfg = PipeCfg<W, G, OPT, VPL>;
+  auto kern = tbe_pipe_update_kernel<W, G, Key, OPT, false, VPL>;
+  if (p.flags & NEO_BWD_FLAG_FULL_ROWS) kern = tbe_pipe_update_kernel<W, G, Key, OPT, true, VPL>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve pipeline shared memory");
+  const int64_t tasks = (p.N + NEO_PIPE_CHUNK - 1) / NEO_PIPE_CHUNK;
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 2 * Cfg::P * kWarp, Cfg::kSmem);
+  if (per_sm < 1) per_sm = 1;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > (tasks + Cfg::P - 1) / Cfg::P) grid = (tasks + Cfg::P - 1) / Cfg::P;
+  if (grid < 1) grid = 1;
+  kern<<<(unsigned)grid, 2 * Cfg::P * kWarp, Cfg::kSmem, s>>>(p);
+  return check_launch("neo_tbe_backward(pipe)");
+}
+
 // ---------------------------------------------------------------------------
 template <typename W, typename G, typename Key, int OPT, int VPL>
 static int launch_stream_vpl(const SegParams& p, cudaStream_t s) {
@@ -779,6 +808,7 @@ static int launch_stream_vpl(const SegParams& p, cudaStream_t s) {
     const int rc = check_launch("neo_tbe_backward(hot chunks)");
     if (rc) return rc;
   }
+  if ((p.flags & NEO_BWD_FLAG_ALIGNED) && use_pipe_variant()) return launch_pipe<W, G, Key, OPT, VPL>(p, s, sms);
   kern<<<(unsigned)grid, kStreamWarps * kWarp, smem, s>>>(p);
   return check_launch("neo_tbe_backward(stream)");
 }
