@@ -69,6 +69,19 @@ def workload_name(a) -> str:
             f"pooling {a.pooling}, row-wise AdaGrad")
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/r1_traffic.json), or None."""
+    f = ROOT / "profiles" / "r1_traffic.json"
+    if kernel is None or not f.exists():
+        return None
+    try:
+        d = json.loads(f.read_text())[kernel]
+        return float(d["dram_read_bytes"] + d["dram_write_bytes"])
+    except Exception:
+        return None
+
+
 def hbm_peak():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -337,7 +350,7 @@ def run_b200(a, rank, world):
     if applies:  # streamed segment-walk + optimizer launches (one per sort group)
         ap_ms = float(np.mean([x.elapsed_time(y) for x, y, _, _ in applies]))
         ap_bytes = float(np.mean([bwd_bytes(U_list[t0:t1], N, D, B) for _, _, t0, t1 in applies]))
-        dominant = ("tbe_stream_update_kernel (segment walk + row-wise AdaGrad, one launch per "
+        dominant = ("tbe_pipe_update_kernel (warp-specialised segment walk + row-wise AdaGrad, one launch per "
                     f"{applies[0][3] - applies[0][2]}-table sort group)", ap_bytes / (ap_ms * 1e-3) / 1e9,
                     ap_bytes, ap_ms)
     else:
@@ -351,9 +364,11 @@ def run_b200(a, rank, world):
                    "l2": "inputs larger than L2 (32.8 GB of tables, 537 MB of ids per step, 2 alternating batches)"},
         "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": dominant[1], "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dominant[1] / peak,
-                     "traffic": None, "algorithmic_bytes": dominant[2], "ms": dominant[3]},
+                     "traffic": ncu_traffic("tbe_pipe_update_kernel" if applies else None),
+                     "traffic_source": "profiles/r1_traffic.json (ncu --set full, one launch)",
+                     "algorithmic_bytes": dominant[2], "ms": dominant[3]},
         "roofline_fwd": {"kernel": "tbe_forward_kernel", "achieved": fwd_gbs, "frac": fwd_gbs / peak, "ms": fwd_ms,
-                         "algorithmic_bytes": fb,
+                         "algorithmic_bytes": fb, "traffic": ncu_traffic("tbe_forward_kernel"),
                          "note": "algorithmic bytes count every lookup's row read; L2 serves the repeated rows, "
                                  "so achieved can exceed the copy peak (ncu DRAM bytes: profiles/)"},
         "roofline_step": {"achieved": step_gbs, "frac": step_gbs / peak, "fwd_gbs": fwd_gbs, "bwd_gbs": bwd_gbs,

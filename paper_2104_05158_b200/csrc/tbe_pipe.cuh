@@ -40,12 +40,18 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_arrive_cp_async(uint32_t bar) {
   asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
+// upper bound on one hardware-suspended wait (the warp wakes as soon as the
+// phase completes); the default limit is short and the retry loop then burns
+// issue slots that the other role's warps need
+#ifndef NEO_PIPE_SUSPEND_NS
+#define NEO_PIPE_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
-      : "r"(bar), "r"(parity)
+      : "r"(bar), "r"(parity), "r"(NEO_PIPE_SUSPEND_NS)
       : "memory");
   return ok != 0;
 }
