@@ -59,6 +59,9 @@ def parse_args(argv=None):
                    help="diagnostic: one backward call over all tables (no shorter sort keys)")
     p.add_argument("--upstream-broadcast", action="store_true",
                    help="diagnostic: one upstream row for every bag (stride 0); not a valid bench number")
+    p.add_argument("--overlap-sort", type=int, default=-1,
+                   help="N=1: issue the backward's key build + sort on a side stream under the forward, with the "
+                        "forward capped at this many CTAs per SM (0 = uncapped; -1 = off)")
     p.add_argument("--cpu-sample-batch", type=int, default=0,
                    help="samples per table in one CPU-baseline sample (default: full batch)")
     return p.parse_args(argv)
@@ -310,8 +313,14 @@ def run_b200(a, rank, world):
 
     counts = None if a.no_subgroups else [N] * T  # host-known per-table id counts (lengths are host data)
 
+    overlap = a.overlap_sort >= 0 and counts is not None
+    if overlap:
+        tbe.set_forward_residency(a.overlap_sort)
+
     def step(i):
         ix = batches[i % 2]
+        if overlap:
+            grp.prepare_backward(ix, offsets, B, upstream, counts, optim="rowwise_adagrad")
         grp.forward(ix, offsets, B, out=out)
         grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS,
                      table_counts=counts)
@@ -330,6 +339,8 @@ def run_b200(a, rank, world):
         e0, e1, e2 = ev[i]
         e0.record()
         ix = batches[i % 2]
+        if overlap:
+            grp.prepare_backward(ix, offsets, B, upstream, counts, optim="rowwise_adagrad")
         grp.forward(ix, offsets, B, out=out)
         e1.record()
         grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS,
@@ -360,6 +371,8 @@ def run_b200(a, rank, world):
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(a), "tables": T, "rows": H, "dim": D, "batch_per_gpu": B,
+                   "backward_sort": (f"side stream under the forward (forward capped at {a.overlap_sort} CTAs/SM)"
+                                     if overlap else "in the backward, serial"),
                    "pooling": L, "index_dtype": "int32", "optimizer": "rowwise_adagrad",
                    "l2": "inputs larger than L2 (32.8 GB of tables, 537 MB of ids per step, 2 alternating batches)"},
         "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": dominant[1], "peak": peak,

@@ -120,6 +120,13 @@ int neo_tbe_forward(int32_t num_tables, int64_t batch,
                     neo_error* err,              /* may be NULL */
                     void* stream);
 
+/* Cap the forward's grid at ctas_per_sm CTAs per SM (grid-stride over bags;
+ * 0 = uncapped, the default).  A capped, DRAM-bound forward leaves SM
+ * resources to a concurrent side-stream kernel, e.g. the next backward's key
+ * build + radix sort (NEO_BWD_FLAG_PREPARE).  Process-wide setting; no
+ * reference counterpart (scheduling knob of this implementation). */
+int neo_set_forward_residency(int32_t ctas_per_sm);
+
 /* Same, with the pooled all-to-all fused into the store: bag row b (of the
  * batch rows) is written to out_ptrs[b / rows_per_dst] at row b %
  * rows_per_dst (out_ptrs: device array of destination base pointers, e.g.

@@ -55,6 +55,7 @@ SIGNATURES = {
         C.c_int,
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I32, I64, P, P],
     ),
+    "neo_set_forward_residency": (C.c_int, [I32]),
     "neo_tbe_forward_scatter": (
         C.c_int,
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I64, I32, I64, P, P],

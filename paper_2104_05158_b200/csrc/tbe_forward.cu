@@ -26,6 +26,8 @@ constexpr int kFwdWarps = 8;   // warps per CTA
 // scatter destination of the current launch (set by neo_tbe_forward_scatter
 // around the dispatch; host-side, per thread)
 static thread_local const uint64_t* g_out_ptrs = nullptr;
+// forward grid cap in CTAs per SM (0 = one CTA per 8 bags, uncapped); process-wide
+static int g_fwd_ctas_per_sm = 0;
 static thread_local int64_t g_rows_per_dst = 1;
 constexpr int kFwdStage = 64;  // row ids staged per warp per pass
 constexpr int kFwdUnroll = 8;  // row gathers in flight per lane
@@ -120,8 +122,11 @@ tbe_forward_kernel(int32_t T, int64_t B, const int64_t* __restrict__ row_offsets
   __shared__ Idx s_idx[kFwdWarps][kFwdStage];
   const int warp = threadIdx.x / kWarp;
   const int lane = threadIdx.x % kWarp;
-  const int64_t bag = (int64_t)blockIdx.x * kFwdWarps + warp;
-  if (bag >= (int64_t)T * B) return;
+  // grid-stride over bags: the grid may be capped (neo_set_forward_residency)
+  // so that a side-stream kernel (the backward's key build + sort) can
+  // co-reside with this DRAM-bound gather
+  for (int64_t bag = (int64_t)blockIdx.x * kFwdWarps + warp; bag < (int64_t)T * B;
+       bag += (int64_t)gridDim.x * kFwdWarps) {
   const int32_t t = (int32_t)(bag / B);
   const int64_t b = bag - (int64_t)t * B;
   const int32_t doff = dim_offsets[t];
@@ -147,6 +152,8 @@ tbe_forward_kernel(int32_t T, int64_t B, const int64_t* __restrict__ row_offsets
   else
     fwd_bag<W, Idx, Out, 1>(wt, D, H, indices, offsets[bag], offsets[bag + 1], s_idx[warp],
                             pooling, orow, err, lane);
+  __syncwarp();
+  }
 }
 
 template <typename W, typename Idx, typename Out>
@@ -197,6 +204,12 @@ static int launch_fwd_idx(int32_t index_dtype, int32_t out_dtype, dim3 grid, cud
 
 }  // namespace neo
 
+extern "C" int neo_set_forward_residency(int32_t ctas_per_sm) {
+  if (ctas_per_sm < 0) return neo::fail(NEO_E_ARG, "neo_set_forward_residency: negative");
+  neo::g_fwd_ctas_per_sm = ctas_per_sm;
+  return NEO_OK;
+}
+
 extern "C" int neo_tbe_forward(int32_t num_tables, int64_t batch, const int64_t* row_offsets,
                                const int32_t* dim_offsets, int32_t max_dim,
                                const uint64_t* weights, int32_t weight_dtype,
@@ -216,7 +229,15 @@ extern "C" int neo_tbe_forward(int32_t num_tables, int64_t batch, const int64_t*
   const int64_t bags = (int64_t)num_tables * batch;
   const int64_t blocks = (bags + kFwdWarps - 1) / kFwdWarps;
   if (blocks > INT_MAX) return fail(NEO_E_ARG, "neo_tbe_forward: too many bags");
-  const dim3 grid((unsigned)blocks);
+  int64_t gblocks = blocks;
+  if (g_fwd_ctas_per_sm > 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t cap = (int64_t)sms * g_fwd_ctas_per_sm;
+    if (gblocks > cap) gblocks = cap;
+  }
+  const dim3 grid((unsigned)gblocks);
   cudaStream_t s = as_stream(stream);
   int rc;
   switch (weight_dtype) {

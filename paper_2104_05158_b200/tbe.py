@@ -215,6 +215,14 @@ class TableGroup:
                 mode_code |= capi.NEO_BWD_FLAG_ALIGNED
                 if all(d == 32 * vec for d in self.dims):
                     mode_code |= capi.NEO_BWD_FLAG_FULL_ROWS
+        prep = getattr(self, "_prepared", None)
+        if (mode == "update" and prep is not None and prep["key"] == (indices.data_ptr(), offsets.data_ptr(), batch)
+                and table_counts is not None):
+            # keys + sorts were issued by prepare_backward (side stream, e.g. under the forward)
+            self._prepared = None
+            self._backward_apply_prepared(prep, indices, offsets, batch, grad, stride, mode_code, optim, lr, eps,
+                                          pooling, err, table_counts, timers)
+            return None
         if mode == "update" and table_counts is not None and self.total_rows >= (1 << SORT_BITS):
             # rows of the whole group need > SORT_BITS key bits: run sub-groups whose
             # rows fit, so each radix sort needs one pass fewer (same results: the
@@ -233,6 +241,79 @@ class TableGroup:
         if mode == "aggregate":
             return out_ids, out_grads, out_count
         return None
+
+    def prepare_backward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, grad: torch.Tensor,
+                         table_counts: Sequence[int], optim: Optional[str] = None, pooling: str = "sum",
+                         err: Optional[ErrorRecord] = None) -> bool:
+        """Issue the key build + radix sort of every sort sub-group of the
+        next UPDATE backward over (indices, offsets) on a side stream, now.
+        They depend on the ids only, so they can run under the forward (cap
+        its residency with set_forward_residency so both fit on the SMs).
+        `grad` is the upstream buffer the backward will receive (only its
+        layout is used here).  The next backward() with the same indices and
+        offsets then runs only the segment walks + optimizer.  Returns False
+        (nothing issued) when the streamed path does not apply."""
+        optim = optim or self.optim or "sgd"
+        stride = grad.stride(0) if grad.dim() == 2 else self.total_dim
+        if not self._streamed(batch, stride, pooling) or self.total_rows < 1:
+            return False
+        groups = self._sort_groups() if self.total_rows >= (1 << SORT_BITS) else [(0, self.T)]
+        if len(groups) == 1 and not hasattr(self, "_group_meta"):
+            self._group_meta = {}
+        if (0, self.T) in groups and (0, self.T) not in self._group_meta:
+            self._group_meta[(0, self.T)] = self.row_offsets
+        mode_code = capi.NEO_BWD_UPDATE | self._layout_flags(grad, stride)
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_prep_side", None) is None:
+            self._prep_side = torch.cuda.Stream(device=self.device)
+        side = self._prep_side
+        side.wait_stream(main)
+        events, wss = [], []
+        with torch.cuda.stream(side):
+            for i, (t0, t1) in enumerate(groups):
+                n = int(sum(table_counts[t0:t1]))
+                rows = int(self.row_offsets_h[t1] - self.row_offsets_h[t0])
+                wsb = capi.lib().neo_tbe_backward_workspace_bytes(max(n, 1), rows, self.max_dim)
+                ws = WORKSPACE.get(f"tbe_bwd_prep{i}", wsb, self.device)
+                if n > 0:
+                    self._backward_call(indices, offsets, batch, grad, stride, mode_code | capi.NEO_BWD_FLAG_PREPARE,
+                                        optim, 0.05, 0.0, pooling, err, t0, t1, table_counts, ws=ws)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                events.append(ev)
+                wss.append(ws)
+        self._prepared = {"key": (indices.data_ptr(), offsets.data_ptr(), batch), "groups": groups,
+                          "events": events, "ws": wss}
+        return True
+
+    def _layout_flags(self, grad: torch.Tensor, stride: int) -> int:
+        vec = 16 // torch.empty(0, dtype=self.dtype).element_size()
+        aligned = (all(d % vec == 0 for d in self.dims) and stride % vec == 0 and grad.data_ptr() % 16 == 0
+                   and all(w is None or w.data_ptr() % 16 == 0 for w in self.weights))
+        flags = 0
+        if aligned:
+            flags |= capi.NEO_BWD_FLAG_ALIGNED
+            if all(d == 32 * vec for d in self.dims):
+                flags |= capi.NEO_BWD_FLAG_FULL_ROWS
+        return flags
+
+    def _backward_apply_prepared(self, prep, indices, offsets, batch, grad, stride, mode_code, optim, lr, eps,
+                                 pooling, err, table_counts, timers):
+        main = torch.cuda.current_stream(self.device)
+        for (t0, t1), ev, ws in zip(prep["groups"], prep["events"], prep["ws"]):
+            main.wait_event(ev)
+            if int(sum(table_counts[t0:t1])) == 0:
+                continue
+            if timers is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(main)
+            self._backward_call(indices, offsets, batch, grad, stride, mode_code | capi.NEO_BWD_FLAG_APPLY, optim,
+                                lr, eps, pooling, err, t0, t1, table_counts, ws=ws)
+            if timers is not None:
+                e1.record(main)
+                timers.setdefault("apply", []).append((e0, e1, t0, t1))
+        # the side stream must not reuse these workspaces before the applies ran
+        self._prep_side.wait_stream(main)
 
     def _sort_groups(self):
         """Consecutive table ranges whose total rows fit SORT_BITS-bit keys."""
@@ -332,6 +413,12 @@ class TableGroup:
 
 # ---------------------------------------------------------------------------
 # layout kernels
+
+
+def set_forward_residency(ctas_per_sm: int) -> None:
+    """Cap the TBE forward at ctas_per_sm CTAs per SM (0 = uncapped) so a
+    side-stream prepare_backward() can co-reside with it."""
+    capi.check(capi.lib().neo_set_forward_residency(int(ctas_per_sm)), "neo_set_forward_residency")
 
 
 def lengths_to_offsets(lengths: torch.Tensor) -> torch.Tensor:

@@ -103,3 +103,36 @@ def test_pipe_matches_stream_bitwise_and_oracle(tbe, case):
         bound = 1e-4 * (np.abs(w) + np.abs(w - init_w[t])) + ulp * np.abs(w) + 1e-6
         assert (np.abs(got - w) <= bound).all(), f"table {t}: max err {np.abs(got - w).max()}"
         col += D
+
+
+def test_prepare_backward_on_side_stream_matches(tbe):
+    """prepare_backward (key build + sort issued early on a side stream, here
+    under a residency-capped forward) + backward == backward alone, bitwise."""
+    rows, dims, B, L = [300000, 200000, 250000], [128, 128, 128], 4096, 16
+    T = len(rows)
+    rng = np.random.default_rng(5)
+    idx = np.concatenate([rng.integers(0, r, size=B * L) for r in rows]).astype(np.int32)
+    ix = torch.from_numpy(idx).cuda()
+    off = torch.arange(0, T * B + 1, dtype=torch.int64, device="cuda") * L
+    up = torch.from_numpy(rng.standard_normal((B, sum(dims))).astype(np.float32)).cuda()
+    counts = [B * L] * T
+    outs = []
+    for prepared in (False, True):
+        grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim="rowwise_adagrad")
+        g = torch.Generator(device="cuda")
+        g.manual_seed(3)
+        grp._storage.copy_(torch.randn(grp._storage.shape, generator=g, device="cuda"))
+        if prepared:
+            tbe.set_forward_residency(3)
+            try:
+                assert grp.prepare_backward(ix, off, B, up, counts, optim="rowwise_adagrad")
+                pooled = grp.forward(ix, off, B)
+            finally:
+                tbe.set_forward_residency(0)
+        else:
+            pooled = grp.forward(ix, off, B)
+        grp.backward(ix, off, B, up, mode="update", optim="rowwise_adagrad", lr=0.05, eps=1e-8, table_counts=counts)
+        torch.cuda.synchronize()
+        outs.append((pooled.clone(), grp._storage.clone(), torch.cat([m.flatten() for m in grp.moments])))
+    for a, b in zip(outs[0], outs[1]):
+        assert torch.equal(a, b)
