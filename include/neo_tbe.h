@@ -248,6 +248,22 @@ int neo_gather_blocks(int32_t n, const uint64_t* src_ptrs, const int64_t* counts
                       const int64_t* dst_offsets, void* dst, int32_t elem_bytes,
                       void* stream);
 
+/* ---- software row cache (cache.py:68-133) -------------------------------
+ * Replays an access trace through a num_sets x ways set-associative cache
+ * (set = row % num_sets) with LRU or LFU replacement exactly as the
+ * reference's sequential access() loop does (cache.py:68-98), on the device:
+ * hit[p] (uint8, may be NULL) and evicted[p] (int64 row or -1, may be NULL)
+ * receive access p's AccessResult; stats[0..2] (device int64) = hits,
+ * misses, evictions (cache.py:117-126 TraceStats).  A negative row is
+ * recorded in err (first position); the reference raises InvalidValue
+ * ("row_id") there.  ways <= 32 (one way per lane).  Replaces
+ * neosim.cache.simulate_trace / access over a trace. */
+enum { NEO_CACHE_LRU = 0, NEO_CACHE_LFU = 1 };
+size_t neo_cache_workspace_bytes(int64_t num_accesses);
+int neo_cache_simulate(int64_t num_sets, int32_t ways, int32_t policy, const int64_t* trace,
+                       int64_t num_accesses, uint8_t* hit, int64_t* evicted, int64_t* stats,
+                       void* workspace, size_t workspace_bytes, neo_error* err, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

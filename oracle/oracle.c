@@ -17,6 +17,10 @@
  *             w -= (lr*g) / (sqrt(m) + eps); zero rows skipped
  *   adagrad   embedding.py:241-246; sgd embedding.py:253
  *   bucketize comms.py:131-140 searchsorted(ends, idx, 'right') + masks
+ *   cache     cache.py:68-98 access(): set = row % num_sets; hit refreshes
+ *             last_used (global clock) and frequency; a miss into a full set
+ *             evicts argmin (last_used, i) [LRU] or (frequency, last_used, i)
+ *             [LFU] and appends the new line
  * Compiled with -ffp-contract=off so no a*b+c is fused.
  */
 #include <math.h>
@@ -153,4 +157,53 @@ int64_t or_bucketize(int64_t n, const int64_t* offsets, const int64_t* idx, int 
     }
   }
   return -1;
+}
+
+
+/* cache.py:68-98 access() over a whole trace (cache.py:117-126
+ * simulate_trace).  Lines of a set are kept in the reference's list order
+ * (append on insert, delete the victim).  Returns the first position with a
+ * negative row (the reference raises there), else -1.  hit/evicted may be
+ * NULL; evicted[p] = -1 when access p evicted nothing. */
+int64_t or_cache_simulate(int64_t num_sets, int64_t ways, int lfu, int64_t n, const int64_t* trace,
+                          uint8_t* hit, int64_t* evicted, int64_t* stats) {
+  int64_t* row = (int64_t*)malloc(sizeof(int64_t) * (size_t)(num_sets * ways));
+  int64_t* last = (int64_t*)malloc(sizeof(int64_t) * (size_t)(num_sets * ways));
+  int64_t* freq = (int64_t*)malloc(sizeof(int64_t) * (size_t)(num_sets * ways));
+  int64_t* len = (int64_t*)calloc((size_t)num_sets, sizeof(int64_t));
+  int64_t hits = 0, misses = 0, evictions = 0, clock = 0, bad = -1;
+  for (int64_t p = 0; p < n; ++p) {
+    const int64_t r = trace[p];
+    if (r < 0) { bad = p; break; }
+    const int64_t s = r % num_sets;
+    int64_t* R = row + s * ways; int64_t* Lu = last + s * ways; int64_t* F = freq + s * ways;
+    clock += 1;
+    int64_t i, found = -1;
+    for (i = 0; i < len[s]; ++i) if (R[i] == r) { found = i; break; }
+    if (found >= 0) {
+      Lu[found] = clock; F[found] += 1; hits += 1;
+      if (hit) hit[p] = 1;
+      if (evicted) evicted[p] = -1;
+      continue;
+    }
+    misses += 1;
+    int64_t ev = -1;
+    if (len[s] >= ways) {
+      int64_t v = 0;
+      for (i = 1; i < len[s]; ++i) {
+        if (lfu) {
+          if (F[i] < F[v] || (F[i] == F[v] && Lu[i] < Lu[v])) v = i;
+        } else if (Lu[i] < Lu[v]) v = i;
+      }
+      ev = R[v];
+      for (i = v; i + 1 < len[s]; ++i) { R[i] = R[i + 1]; Lu[i] = Lu[i + 1]; F[i] = F[i + 1]; }
+      len[s] -= 1; evictions += 1;
+    }
+    R[len[s]] = r; Lu[len[s]] = clock; F[len[s]] = 1; len[s] += 1;
+    if (hit) hit[p] = 0;
+    if (evicted) evicted[p] = ev;
+  }
+  stats[0] = hits; stats[1] = misses; stats[2] = evictions;
+  free(row); free(last); free(freq); free(len);
+  return bad;
 }

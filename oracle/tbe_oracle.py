@@ -48,6 +48,8 @@ def lib():
         h.or_apply_f64.argtypes = [C.c_int, _I, _P, _P, _I, _P, _P, C.c_double, C.c_double]
         h.or_bucketize.restype = _I
         h.or_bucketize.argtypes = [_I, _P, _P, C.c_int, _P, _P, _P]
+        h.or_cache_simulate.restype = _I
+        h.or_cache_simulate.argtypes = [_I, _I, C.c_int, _I, _P, _P, _P, _P]
         _lib = h
     return _lib
 
@@ -332,3 +334,17 @@ def neot_read(fh):
     elif mcode == 2:
         moment = np.frombuffer(fh.read(rows * dim * 8), dtype=np.float64).reshape(rows, dim).copy()
     return values, moment, prec
+
+
+def cache_simulate_c(num_sets: int, ways: int, policy: str, trace):
+    """cache.py:68-126 (access over a trace): (hit uint8[n], evicted int64[n],
+    (hits, misses, evictions)); raises OracleIndexError at a negative row."""
+    tr = np.ascontiguousarray(trace, dtype=np.int64)
+    n = len(tr)
+    hit = np.zeros(max(n, 1), dtype=np.uint8)
+    ev = np.zeros(max(n, 1), dtype=np.int64)
+    st = np.zeros(3, dtype=np.int64)
+    bad = lib().or_cache_simulate(num_sets, ways, 1 if policy == "lfu" else 0, n, _p(tr), _p(hit), _p(ev), _p(st))
+    if bad >= 0:
+        raise OracleIndexError(int(bad), int(tr[bad]))
+    return hit[:n], ev[:n], tuple(int(x) for x in st)

@@ -16,7 +16,7 @@ from __future__ import annotations
 __version__ = "0.1.0"
 
 from . import _capi
-from . import checkpoint  # noqa: F401
+from . import cache, checkpoint  # noqa: F401
 from .errors import (IndexOutOfRange, InvalidScheme, InvalidValue, LayoutMismatch,  # noqa: F401
                      MalformedDocument, MissingKey, NeosimError, NonMonotonicOffsets)
 from .spec import (CombinedBatch, EmbeddingTable, GlobalBatchLayout, IndexSkew, LayoutTag,  # noqa: F401

@@ -22,6 +22,7 @@ NEO_OPT_SGD, NEO_OPT_ROWWISE_ADAGRAD, NEO_OPT_ADAGRAD, NEO_OPT_NONE = 0, 1, 2, 3
 NEO_BWD_UPDATE, NEO_BWD_AGGREGATE, NEO_BWD_DENSE = 0, 1, 2
 NEO_BWD_FLAG_ALIGNED, NEO_BWD_FLAG_FULL_ROWS = 0x100, 0x200
 NEO_BWD_FLAG_PREPARE, NEO_BWD_FLAG_APPLY = 0x400, 0x800
+NEO_CACHE_LRU, NEO_CACHE_LFU = 0, 1
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -56,6 +57,8 @@ SIGNATURES = {
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I32, I64, P, P],
     ),
     "neo_set_forward_residency": (C.c_int, [I32]),
+    "neo_cache_workspace_bytes": (SZ, [I64]),
+    "neo_cache_simulate": (C.c_int, [I64, I32, I32, P, I64, P, P, P, P, SZ, P, P]),
     "neo_tbe_forward_scatter": (
         C.c_int,
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I64, I32, I64, P, P],

@@ -14,6 +14,8 @@ wherever the reference binds it:
   train_step_sharded, reassemble_values, plus the names comms.py binds from
   embedding at import (comms.py:18-28);
 * ``neosim.cli``: train_step_reference / train_step_sharded (cli.py:25-26);
+* ``neosim.cache.simulate_trace`` (cache.py:117-126; bound by name in
+  cli.py:24 and re-exported by neosim/__init__.py:87);
 * the ``neosim`` package re-exports (neosim/__init__.py:60-86).
 
 Errors raised by this package are aliased to the reference's exception
@@ -24,6 +26,7 @@ from __future__ import annotations
 
 import importlib
 
+from . import cache as _cache
 from . import comms as _comms
 from . import embedding as _emb
 from . import errors as _errors
@@ -36,7 +39,7 @@ _COMMS = ["bucketize_rowwise", "replicate_columnwise", "to_wtb", "permute_WTB_to
 _COMMS_FROM_EMB = ["apply_optimizer", "backward_sort_aggregate", "forward_pooled", "merge_row_gradients",
                    "storage_roundtrip"]
 _ERRORS = ["NeosimError", "MalformedDocument", "MissingKey", "InvalidValue", "NonMonotonicOffsets",
-           "InvalidScheme", "IndexOutOfRange", "LayoutMismatch"]
+           "InvalidScheme", "IndexOutOfRange", "LayoutMismatch", "EmptyTrace"]
 
 _saved: list = []
 
@@ -54,10 +57,11 @@ def install(neosim=None):
     com = importlib.import_module(neosim.__name__ + ".comms")
     cli = importlib.import_module(neosim.__name__ + ".cli")
     ref_err = importlib.import_module(neosim.__name__ + ".errors")
+    ref_cache = importlib.import_module(neosim.__name__ + ".cache")
     # our errors become the reference's classes (raised and caught as such)
     from . import _capi, dist, plan, spec, tbe
 
-    for mod in (_errors, _emb, _comms, tbe, spec, plan, dist):
+    for mod in (_errors, _emb, _comms, _cache, tbe, spec, plan, dist):
         for name in _ERRORS:
             if hasattr(mod, name):
                 _set(mod, name, getattr(ref_err, name))
@@ -78,6 +82,11 @@ def install(neosim=None):
             _set(neosim, name, getattr(_comms, name))
     for name in _COMMS_FROM_EMB:
         _set(com, name, getattr(_emb, name))
+    _set(_cache, "TraceStats", ref_cache.TraceStats)
+    _set(ref_cache, "simulate_trace", _cache.simulate_trace)
+    if hasattr(neosim, "simulate_trace"):
+        _set(neosim, "simulate_trace", _cache.simulate_trace)
+    _set(cli, "simulate_trace", _cache.simulate_trace)
     _set(cli, "train_step_reference", _emb.train_step_reference)
     _set(cli, "train_step_sharded", _comms.train_step_sharded)
     _capi.lib()  # fail loudly now if the native library is missing

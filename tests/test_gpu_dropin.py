@@ -139,3 +139,30 @@ def test_reference_cli_verify_through_dropin(ref, tmp_path):
         assert rc == 0
         body = json.loads((out / "verify.json").read_text())["body"]
         assert body["passed"] and body["max_deviation"] <= 1e-9
+
+
+def test_cache_simulate_trace_patched(ref):
+    """neosim.cache.simulate_trace (and its by-name bindings in cli.py and the
+    package) route to the GPU replay and return the reference's TraceStats."""
+    neosim, _ = ref
+    from neosim import cache as rc, cli
+
+    from paper_2104_05158_b200 import cache as ours
+
+    assert rc.simulate_trace is ours.simulate_trace and cli.simulate_trace is ours.simulate_trace
+    rng = np.random.default_rng(9)
+    for pol in (rc.ReplacementPolicy.LRU, rc.ReplacementPolicy.LFU):
+        cfg = rc.CacheConfig(num_sets=8, ways=4, policy=pol)
+        tr = rng.integers(0, 200, 5000).tolist()
+        st = rc.simulate_trace(cfg, tr)
+        state = rc.CacheState(cfg)  # the reference's own sequential loop as the checker
+        for r in tr:
+            rc.access(state, r)
+        assert isinstance(st, rc.TraceStats)
+        assert (st.hits, st.misses, st.evictions) == (state.hits, state.misses, state.evictions)
+    with pytest.raises(neosim.EmptyTrace):
+        rc.simulate_trace(rc.CacheConfig(num_sets=2), [])
+    shipped = rc.make_scan_hot_trace()
+    lru = rc.simulate_trace(rc.CacheConfig(num_sets=4, ways=8, policy=rc.ReplacementPolicy.LRU), shipped)
+    lfu = rc.simulate_trace(rc.CacheConfig(num_sets=4, ways=8, policy=rc.ReplacementPolicy.LFU), shipped)
+    assert lfu.hit_rate > lru.hit_rate  # test_cache.py:97-106
