@@ -62,6 +62,7 @@ def parse_args(argv=None):
     p.add_argument("--overlap-sort", type=int, default=-1,
                    help="N=1: issue the backward's key build + sort on a side stream under the forward, with the "
                         "forward capped at this many CTAs per SM (0 = uncapped; -1 = off)")
+    p.add_argument("--no-cache-bench", action="store_true", help="skip the software row-cache replay line")
     p.add_argument("--cpu-sample-batch", type=int, default=0,
                    help="samples per table in one CPU-baseline sample (default: full batch)")
     return p.parse_args(argv)
@@ -214,6 +215,52 @@ class CpuPool:
     def close(self):
         self.pool.close()
         self.pool.join()
+
+
+def cache_replay_bench(dev, cpu: bool = True) -> dict:
+    """the software row cache (cache.py:68-126).  A Zipf
+    (alpha 1.05) trace of 64 M row accesses over 100 M rows replayed through a
+    1 M-set x 32-way LRU cache (32 M resident rows, the HBM tier of config 4)
+    on the GPU, inputs resident; CPU: the oracle's C port of the reference's
+    sequential access() loop on a 4 M-access prefix, one core."""
+    import torch
+
+    from paper_2104_05158_b200 import cache
+
+    n, sets, ways = 64 << 20, 1 << 20, 32
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+    u = torch.rand(n, generator=g, device=dev, dtype=torch.float64)
+    # inverse-CDF Zipf-like ranks over 1e8 rows (continuous approximation, alpha 1.05)
+    alpha, H = 1.05, 1e8
+    tr = torch.clamp((1.0 - u * (1.0 - H ** (1.0 - alpha))) ** (1.0 / (1.0 - alpha)) - 1.0, 0, H - 1).to(torch.int64)
+    cfg = cache.CacheConfig(num_sets=sets, ways=ways)
+    for _ in range(2):
+        _, _, st = cache.access_trace(cfg, tr, with_results=False, device=dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 3
+    e0.record()
+    for _ in range(reps):
+        _, _, st = cache.access_trace(cfg, tr, with_results=True, device=dev)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    out = {"workload": f"{n:,} Zipf(1.05) accesses over 1e8 rows, {sets:,} sets x {ways} ways LRU, per-access "
+                       "AccessResult written (hit, evicted)", "value": n / (ms * 1e-3), "unit": "accesses/s",
+           "ms": ms, "hit_rate": st.hit_rate, "gpu_kernels": "cache_keys_kernel + CUB radix sort + select + "
+                                                              "cache_replay_kernel (warp per set)"}
+    if cpu:
+        from oracle import tbe_oracle as O
+
+        m = 4 << 20
+        sample = tr[:m].cpu().numpy()
+        t0 = time.perf_counter()
+        O.cache_simulate_c(sets, ways, "lru", sample)
+        dt = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": m / dt, "unit": "accesses/s", "cores": 1, "kind": "port",
+                               "sample": f"first {m:,} accesses, oracle C port of cache.py access() (sequential)"}
+    return out
 
 
 def cpu_baseline(a, T_total) -> dict:
@@ -392,6 +439,8 @@ def run_b200(a, rank, world):
     }
     if not a.no_e2e:
         line["e2e"] = e2e_b200(a, grp, dev)
+    if not a.no_cache_bench:
+        line["cache_replay"] = cache_replay_bench(dev, cpu=not a.no_cpu_baseline)
     if not a.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(a, T)
     print(json.dumps(line), flush=True)
