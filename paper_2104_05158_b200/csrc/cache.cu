@@ -12,7 +12,9 @@
 // matters.  So: (1) a stable radix sort of (set, position) pairs groups each
 // set's accesses in trace order; (2) one warp per set replays them, lane w
 // holding way w (row, last_used = position + 1, frequency) in registers; a
-// hit is one ballot, the victim one or two __reduce_min_sync.  Per-access
+// hit is one ballot, the victim one or two __reduce_min_sync; a run of
+// accesses repeating the previous access's row (hot rows) is applied in one
+// step.  Per-access
 // results (hit, evicted row) land at the access's trace position, so the
 // output equals the reference's sequential AccessResult stream.
 #include <climits>
@@ -60,14 +62,42 @@ cache_replay_kernel(const int64_t* __restrict__ trace, const int32_t* __restrict
     uint32_t last = 0, freq = 0;
     bool valid = false;
     int cnt = 0;
+    int64_t prev_r = -1;  // row of the set's previous access (resident after it)
     for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
       const int mm = (int)min64(kWarp, s1 - j0);
       const int32_t my_p = lane < mm ? pos[j0 + lane] : 0;
-      const int64_t my_r = lane < mm ? trace[my_p] : 0;
-      for (int k = 0; k < mm; ++k) {
+      const int64_t my_r = lane < mm ? trace[my_p] : -2;
+      // runs of one row: an access repeating the previous access's row is a
+      // hit on the way that row occupies (hot rows of skewed traces), so a
+      // run of L such accesses is applied at once: frequency += L,
+      // last_used = the run's last clock
+      int64_t up = __shfl_up_sync(full, my_r, 1);
+      if (lane == 0) up = prev_r;
+      const unsigned same = __ballot_sync(full, lane < mm && my_r == up);
+      prev_r = __shfl_sync(full, my_r, mm - 1);
+      for (int k = 0; k < mm;) {
+        if ((same >> k) & 1u) {
+          const unsigned rest = ~(same >> k);  // first access after the run
+          const int L = min(rest ? __ffs(rest) - 1 : kWarp - k, mm - k);
+          const int64_t r = __shfl_sync(full, my_r, k);
+          const uint32_t clock_end = (uint32_t)__shfl_sync(full, my_p, k + L - 1) + 1u;
+          const unsigned hm = __ballot_sync(full, valid && row == r);
+          if (lane == __ffs(hm) - 1) {
+            last = clock_end;
+            freq += (uint32_t)L;
+          }
+          if (lane >= k && lane < k + L) {
+            if (hit_out) hit_out[my_p] = 1;
+            if (ev_out) ev_out[my_p] = -1;
+          }
+          h += (unsigned long long)L;
+          k += L;
+          continue;
+        }
         const int32_t p = __shfl_sync(full, my_p, k);
         const int64_t r = __shfl_sync(full, my_r, k);
         const uint32_t clock = (uint32_t)p + 1u;
+        ++k;
         const unsigned hm = __ballot_sync(full, valid && row == r);
         if (hm) {
           if (lane == __ffs(hm) - 1) {
