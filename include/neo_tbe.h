@@ -264,6 +264,29 @@ int neo_cache_simulate(int64_t num_sets, int32_t ways, int32_t policy, const int
                        int64_t num_accesses, uint8_t* hit, int64_t* evicted, int64_t* stats,
                        void* workspace, size_t workspace_bytes, neo_error* err, void* stream);
 
+/* ---- HBM tier over host-resident tables -------------
+ * One table: rows (row_bytes each, optimizer state moment_bytes each, 0 for
+ * SGD) live in host memory the device can address (pinned, UVA); an HBM
+ * cache of num_sets x ways slots (cache_weights / cache_moments, slot-major)
+ * holds the rows in use.  neo_tier_prepare maps the batch's ids to slots
+ * (slots_out, int32, same order as ids), writing evicted slots back to host
+ * and fetching missing rows; rows the batch uses are never evicted by it.
+ * tags[num_sets*ways] (int64 row or -1) and stamps[...] (uint32, 0 = never)
+ * are the caller-owned directory; stamp = this batch's number (>= 1,
+ * increasing).  counters[4] (device int64) = misses, write-backs, accesses
+ * that found no free way (set overflow: slot -1), transfers.  Out-of-range
+ * ids are recorded in err.  neo_tier_flush writes every cached row back.
+ * No reference counterpart: the reference models this tier analytically
+ * (cache.py:129-136 effective_row_bandwidth, planner.py:512-522 hbm+dram). */
+size_t neo_tier_workspace_bytes(int64_t num_ids);
+int neo_tier_prepare(int64_t num_rows, int64_t num_sets, int32_t ways, const void* ids, int32_t index_dtype,
+                     int64_t num_ids, int64_t* tags, uint32_t* stamps, uint32_t stamp, void* cache_weights,
+                     void* cache_moments, void* host_weights, void* host_moments, int64_t row_bytes,
+                     int64_t moment_bytes, int32_t* slots_out, int64_t* counters, void* workspace,
+                     size_t workspace_bytes, neo_error* err, void* stream);
+int neo_tier_flush(int64_t num_slots, const int64_t* tags, const void* cache_weights, const void* cache_moments,
+                   void* host_weights, void* host_moments, int64_t row_bytes, int64_t moment_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,6 +59,10 @@ SIGNATURES = {
     "neo_set_forward_residency": (C.c_int, [I32]),
     "neo_cache_workspace_bytes": (SZ, [I64]),
     "neo_cache_simulate": (C.c_int, [I64, I32, I32, P, I64, P, P, P, P, SZ, P, P]),
+    "neo_tier_workspace_bytes": (SZ, [I64]),
+    "neo_tier_prepare": (C.c_int, [I64, I64, I32, P, I32, I64, P, P, C.c_uint32, P, P, P, P, I64, I64, P, P, P, SZ,
+                                   P, P]),
+    "neo_tier_flush": (C.c_int, [I64, P, P, P, P, P, I64, I64, P]),
     "neo_tbe_forward_scatter": (
         C.c_int,
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I64, I32, I64, P, P],

@@ -219,3 +219,260 @@ extern "C" int neo_cache_simulate(int64_t num_sets, int32_t ways, int32_t policy
   if (rc) return rc;
   return NEO_OK;
 }
+
+// ===========================================================================
+// HBM tier over host-resident tables: the embedding rows
+// live in pinned host memory (device-addressable through UVA); an HBM cache
+// of num_sets x ways slots per table holds the rows a batch touches, and the
+// TBE kernels run on the slots.  Per batch:
+//   1. stable radix sort of (set = id % num_sets, position);
+//   2. one warp per set (lane = way): pass 1 stamps every way whose row the
+//      batch uses; pass 2 maps each access to its slot, filling misses into
+//      ways NOT used by this batch (least recently stamped, lowest way on
+//      ties) and queueing (slot, evicted row, fetched row) transfers.  Rows
+//      a batch uses are never evicted by it, so no row is both written back
+//      and fetched in one batch;
+//   3. one warp per transfer writes the evicted slot (row + optimizer state)
+//      back to host memory, then fetches the new row into the slot.
+// A set that needs more than `ways` distinct rows in one batch cannot be
+// served: its extra accesses map to slot -1 and counters[2] counts them.
+// Training through the tier is bitwise identical to training with the whole
+// table in HBM: the same rows, in the same per-row order, feed the same
+// kernels.
+
+namespace neo {
+
+template <typename Idx>
+__global__ void tier_keys_kernel(const Idx* __restrict__ ids, int64_t n, int64_t H, int64_t num_sets,
+                                 uint32_t* __restrict__ keys, int32_t* __restrict__ pos, neo_error* err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = (int64_t)ids[i];
+    const bool ok = r >= 0 && r < H;
+    if (!ok) record_bad_index(err, i);
+    keys[i] = (uint32_t)(ok ? r % num_sets : 0);
+    pos[i] = (int32_t)i;
+  }
+}
+
+template <typename Idx>
+__global__ void __launch_bounds__(256)
+tier_assign_kernel(const Idx* __restrict__ ids, const int32_t* __restrict__ pos, const int32_t* __restrict__ starts,
+                   const int64_t* __restrict__ num_segs, int64_t n, int64_t H, int64_t num_sets, int32_t ways,
+                   int64_t* __restrict__ tags, uint32_t* __restrict__ stamps, uint32_t stamp,
+                   int32_t* __restrict__ slots_out, int64_t* __restrict__ xfer,
+                   unsigned long long* __restrict__ counters) {
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / kWarp;
+  const int64_t S = *num_segs;
+  unsigned long long misses = 0, wbs = 0, over = 0;
+  for (int64_t seg = warp; seg < S; seg += nwarps) {
+    const int64_t s0 = starts[seg];
+    const int64_t s1 = seg + 1 < S ? (int64_t)starts[seg + 1] : n;
+    const int64_t r0 = (int64_t)ids[pos[s0]];
+    // out-of-range ids were keyed to set 0 (and are skipped per access below)
+    const int64_t set_id = (r0 >= 0 && r0 < H) ? r0 % num_sets : 0;
+    const int64_t base = set_id * ways;
+    int64_t tag = lane < ways ? tags[base + lane] : -2;
+    uint32_t st = lane < ways ? stamps[base + lane] : 0xffffffffu;
+    // pass 1: stamp the ways this batch uses
+    for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
+      const int mm = (int)min64(kWarp, s1 - j0);
+      const int64_t my_r = lane < mm ? (int64_t)ids[pos[j0 + lane]] : -1;
+      for (int k = 0; k < mm; ++k) {
+        const int64_t r = __shfl_sync(full, my_r, k);
+        if (tag == r && r >= 0) st = stamp;
+      }
+    }
+    // pass 2: map every access to its slot, filling misses
+    for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
+      const int mm = (int)min64(kWarp, s1 - j0);
+      const int32_t my_p = lane < mm ? pos[j0 + lane] : 0;
+      const int64_t my_r = lane < mm ? (int64_t)ids[my_p] : -1;
+      for (int k = 0; k < mm; ++k) {
+        const int64_t r = __shfl_sync(full, my_r, k);
+        const int32_t p = __shfl_sync(full, my_p, k);
+        if (r < 0 || r >= H) {  // reported through err by the key kernel
+          if (lane == 0) slots_out[p] = -1;
+          continue;
+        }
+        const unsigned hm = __ballot_sync(full, tag == r);
+        if (hm) {
+          if (lane == 0) slots_out[p] = (int32_t)(base + __ffs(hm) - 1);
+          continue;
+        }
+        const bool cand = lane < ways && st != stamp;
+        const unsigned cm = __ballot_sync(full, cand);
+        if (!cm) {
+          ++over;
+          if (lane == 0) slots_out[p] = -1;
+          continue;
+        }
+        const uint32_t smin = __reduce_min_sync(full, cand ? st : 0xffffffffu);
+        const int v = __ffs(__ballot_sync(full, cand && st == smin)) - 1;
+        const int64_t old = __shfl_sync(full, tag, v);
+        ++misses;
+        if (old >= 0) ++wbs;
+        if (lane == v) {
+          tag = r;
+          st = stamp;
+        }
+        if (lane == 0) {
+          const unsigned long long x = atomicAdd(counters + 3, 1ull);
+          xfer[3 * x + 0] = base + v;
+          xfer[3 * x + 1] = old;
+          xfer[3 * x + 2] = r;
+          slots_out[p] = (int32_t)(base + v);
+        }
+      }
+    }
+    if (lane < ways) {
+      tags[base + lane] = tag;
+      stamps[base + lane] = st;
+    }
+  }
+  if (lane == 0 && (misses | wbs | over)) {
+    atomicAdd(counters + 0, misses);
+    atomicAdd(counters + 1, wbs);
+    atomicAdd(counters + 2, over);
+  }
+}
+
+// copy `bytes` (a multiple of 4) from src to dst with the warp's lanes
+__device__ __forceinline__ void warp_copy(void* dst, const void* src, int64_t bytes, int lane) {
+  if ((bytes & 15) == 0 && aligned16(dst) && aligned16(src)) {
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    for (int64_t i = lane; i < bytes / 16; i += kWarp) d[i] = s[i];
+  } else {
+    unsigned* d = reinterpret_cast<unsigned*>(dst);
+    const unsigned* s = reinterpret_cast<const unsigned*>(src);
+    for (int64_t i = lane; i < bytes / 4; i += kWarp) d[i] = s[i];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+tier_transfer_kernel(const int64_t* __restrict__ xfer, const unsigned long long* __restrict__ counters,
+                     unsigned char* cache_w, unsigned char* cache_m, unsigned char* host_w, unsigned char* host_m,
+                     int64_t row_bytes, int64_t mom_bytes) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / kWarp;
+  const int64_t nx = (int64_t)counters[3];
+  for (int64_t i = warp; i < nx; i += nwarps) {
+    const int64_t slot = xfer[3 * i], old = xfer[3 * i + 1], r = xfer[3 * i + 2];
+    if (old >= 0) {  // write back the evicted row and its optimizer state
+      warp_copy(host_w + old * row_bytes, cache_w + slot * row_bytes, row_bytes, lane);
+      if (mom_bytes) warp_copy(host_m + old * mom_bytes, cache_m + slot * mom_bytes, mom_bytes, lane);
+    }
+    warp_copy(cache_w + slot * row_bytes, host_w + r * row_bytes, row_bytes, lane);
+    if (mom_bytes) warp_copy(cache_m + slot * mom_bytes, host_m + r * mom_bytes, mom_bytes, lane);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+tier_flush_kernel(int64_t num_slots, const int64_t* __restrict__ tags, const unsigned char* cache_w,
+                  const unsigned char* cache_m, unsigned char* host_w, unsigned char* host_m, int64_t row_bytes,
+                  int64_t mom_bytes) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / kWarp;
+  for (int64_t slot = warp; slot < num_slots; slot += nwarps) {
+    const int64_t r = tags[slot];
+    if (r < 0) continue;
+    warp_copy(host_w + r * row_bytes, cache_w + slot * row_bytes, row_bytes, lane);
+    if (mom_bytes) warp_copy(host_m + r * mom_bytes, cache_m + slot * mom_bytes, mom_bytes, lane);
+  }
+}
+
+static size_t tier_ws(int64_t n) { return cache_ws(n) + a256(3 * 8 * (size_t)n); }
+
+static unsigned sm_grid(int64_t warps_wanted) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t blocks = (warps_wanted + 7) / 8;
+  return (unsigned)(blocks < 1 ? 1 : (blocks < (int64_t)sms * 8 ? blocks : (int64_t)sms * 8));
+}
+
+}  // namespace neo
+
+extern "C" size_t neo_tier_workspace_bytes(int64_t num_ids) { return neo::tier_ws(num_ids < 1 ? 1 : num_ids); }
+
+extern "C" int neo_tier_prepare(int64_t num_rows, int64_t num_sets, int32_t ways, const void* ids,
+                                int32_t index_dtype, int64_t num_ids, int64_t* tags, uint32_t* stamps,
+                                uint32_t stamp, void* cache_weights, void* cache_moments, void* host_weights,
+                                void* host_moments, int64_t row_bytes, int64_t moment_bytes, int32_t* slots_out,
+                                int64_t* counters, void* workspace, size_t workspace_bytes, neo_error* err,
+                                void* stream) {
+  using namespace neo;
+  cudaStream_t s = as_stream(stream);
+  if (num_rows < 1 || num_sets < 1 || num_sets > (int64_t)UINT32_MAX) return fail(NEO_E_ARG, "num_sets/num_rows");
+  if (ways < 1 || ways > kWarp) return fail(NEO_E_ARG, "ways: 1..32 (one way per lane)");
+  if (index_dtype != NEO_I32 && index_dtype != NEO_I64) return fail(NEO_E_ARG, "index dtype must be I32 or I64");
+  if (num_ids < 0 || num_ids >= INT_MAX) return fail(NEO_E_ARG, "num_ids: 0 .. 2^31-1");
+  if (row_bytes < 4 || (row_bytes & 3) || (moment_bytes & 3) || stamp == 0)
+    return fail(NEO_E_ARG, "row/moment bytes must be multiples of 4; stamp >= 1");
+  if (!tags || !stamps || !cache_weights || !host_weights || !slots_out || !counters)
+    return fail(NEO_E_ARG, "neo_tier_prepare: null pointer");
+  if (cudaMemsetAsync(counters, 0, 4 * sizeof(int64_t), s) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tier_prepare: memset failed");
+  const int64_t n = num_ids;
+  if (n == 0) return NEO_OK;
+  if (workspace_bytes < tier_ws(n)) return fail(NEO_E_ARG, "neo_tier_prepare: workspace too small");
+  unsigned char* w = static_cast<unsigned char*>(workspace);
+  uint32_t* k0 = reinterpret_cast<uint32_t*>(w); w += a256(4 * (size_t)n);
+  uint32_t* k1 = reinterpret_cast<uint32_t*>(w); w += a256(4 * (size_t)n);
+  int32_t* v0 = reinterpret_cast<int32_t*>(w); w += a256(4 * (size_t)n);
+  int32_t* v1 = reinterpret_cast<int32_t*>(w); w += a256(4 * (size_t)n);
+  int32_t* starts = reinterpret_cast<int32_t*>(w); w += a256(4 * (size_t)n);
+  int64_t* nseg = reinterpret_cast<int64_t*>(w); w += a256(8);
+  void* temp = w; w += a256(cub_bytes(n));
+  int64_t* xfer = reinterpret_cast<int64_t*>(w);
+  const unsigned kgrid = (unsigned)min64((n + 255) / 256, 148 * 32);
+  if (index_dtype == NEO_I32)
+    tier_keys_kernel<int32_t><<<kgrid, 256, 0, s>>>((const int32_t*)ids, n, num_rows, num_sets, k0, v0, err);
+  else
+    tier_keys_kernel<int64_t><<<kgrid, 256, 0, s>>>((const int64_t*)ids, n, num_rows, num_sets, k0, v0, err);
+  int rc = check_launch("neo_tier_prepare(keys)");
+  if (rc) return rc;
+  int bits = 1;
+  while (bits < 32 && (uint64_t(1) << bits) < (uint64_t)num_sets) ++bits;
+  size_t tb = cub_bytes(n);
+  cub::DoubleBuffer<uint32_t> kbuf(k0, k1);
+  cub::DoubleBuffer<int32_t> vbuf(v0, v1);
+  if (cub::DeviceRadixSort::SortPairs(temp, tb, kbuf, vbuf, (int)n, 0, bits, s) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tier_prepare: radix sort failed");
+  tb = cub_bytes(n);
+  cub::CountingInputIterator<int32_t> it(0);
+  if (cub::DeviceSelect::If(temp, tb, it, starts, nseg, (int)n, CacheHead{kbuf.Current()}, s) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tier_prepare: segment select failed");
+  auto* cnt = reinterpret_cast<unsigned long long*>(counters);
+  const unsigned agrid = sm_grid(min64(n, num_sets));
+  if (index_dtype == NEO_I32)
+    tier_assign_kernel<int32_t><<<agrid, 256, 0, s>>>((const int32_t*)ids, vbuf.Current(), starts, nseg, n, num_rows,
+                                                       num_sets, ways, tags, stamps, stamp, slots_out, xfer, cnt);
+  else
+    tier_assign_kernel<int64_t><<<agrid, 256, 0, s>>>((const int64_t*)ids, vbuf.Current(), starts, nseg, n, num_rows,
+                                                       num_sets, ways, tags, stamps, stamp, slots_out, xfer, cnt);
+  rc = check_launch("neo_tier_prepare(assign)");
+  if (rc) return rc;
+  tier_transfer_kernel<<<sm_grid(n), 256, 0, s>>>(xfer, cnt, (unsigned char*)cache_weights,
+                                                   (unsigned char*)cache_moments, (unsigned char*)host_weights,
+                                                   (unsigned char*)host_moments, row_bytes, moment_bytes);
+  return check_launch("neo_tier_prepare(transfer)");
+}
+
+extern "C" int neo_tier_flush(int64_t num_slots, const int64_t* tags, const void* cache_weights,
+                              const void* cache_moments, void* host_weights, void* host_moments, int64_t row_bytes,
+                              int64_t moment_bytes, void* stream) {
+  using namespace neo;
+  if (num_slots < 0 || row_bytes < 4 || (row_bytes & 3) || (moment_bytes & 3))
+    return fail(NEO_E_ARG, "neo_tier_flush: bad sizes");
+  if (num_slots == 0) return NEO_OK;
+  tier_flush_kernel<<<sm_grid(num_slots), 256, 0, as_stream(stream)>>>(
+      num_slots, tags, (const unsigned char*)cache_weights, (const unsigned char*)cache_moments,
+      (unsigned char*)host_weights, (unsigned char*)host_moments, row_bytes, moment_bytes);
+  return check_launch("neo_tier_flush");
+}

@@ -1,0 +1,122 @@
+"""HBM tier over host-resident embedding tables.
+
+The reference sizes this tier analytically: a plan whose shards exceed HBM is
+classified ``hbm+dram`` (planner.py:512-522) and served at the harmonic blend
+of the two bandwidths (cache.py:129-136), with a 32-way set-associative row
+cache (cache.py:17-98) deciding residency.  Here the tier is real: each
+table's rows and optimizer state live in pinned host memory that the GPU
+addresses directly (UVA), a ``num_sets x ways`` slot cache per table lives in
+HBM as an ordinary ``TableGroup``, and every batch is mapped onto slots by
+``neo_tier_prepare`` (csrc/cache.cu) before the unchanged TBE forward and
+fused backward run on the slots.  Evicted rows (values + moments) are written
+back, missing rows fetched, in the same stream.  Rows a batch uses are never
+evicted by it, so results are bitwise identical to training with the whole
+table in HBM (tests/test_gpu_tier.py).
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _capi as capi
+from .errors import InvalidValue
+from .tbe import INDEX_CODE, WORKSPACE, ErrorRecord, TableGroup, _stream, raise_if_bad
+
+
+class TieredTableGroup:
+    def __init__(self, rows: Sequence[int], dims: Sequence[int], num_sets, ways: int = 32,
+                 dtype=torch.float32, optim: str = "rowwise_adagrad", device=None,
+                 table_ids: Optional[Sequence[str]] = None):
+        if ways < 1 or ways > 32:
+            raise InvalidValue("ways", "1..32 (one way per lane)")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.rows, self.dims, self.T = [int(r) for r in rows], [int(d) for d in dims], len(rows)
+        self.num_sets = [int(num_sets)] * self.T if np.isscalar(num_sets) else [int(s) for s in num_sets]
+        self.ways, self.optim, self.dtype = ways, optim, dtype
+        self.table_ids = list(table_ids) if table_ids else [f"t{i}" for i in range(self.T)]
+        slots = [s * ways for s in self.num_sets]
+        self.cache = TableGroup(slots, self.dims, dtype=dtype, optim=optim, device=self.device)
+        esz = torch.empty(0, dtype=dtype).element_size()
+        self.row_bytes = [d * esz for d in self.dims]
+        acc = self.cache.acc
+        if optim == "rowwise_adagrad":
+            self.host_m = [torch.zeros(r, dtype=acc, pin_memory=True) for r in self.rows]
+            self.mom_bytes = [torch.empty(0, dtype=acc).element_size()] * self.T
+        elif optim == "adagrad":
+            self.host_m = [torch.zeros((r, d), dtype=acc, pin_memory=True) for r, d in zip(self.rows, self.dims)]
+            self.mom_bytes = [d * torch.empty(0, dtype=acc).element_size() for d in self.dims]
+        else:
+            self.host_m = [None] * self.T
+            self.mom_bytes = [0] * self.T
+        self.host_w = [torch.zeros((r, d), dtype=dtype, pin_memory=True) for r, d in zip(self.rows, self.dims)]
+        self.tags = [torch.full((n,), -1, dtype=torch.int64, device=self.device) for n in slots]
+        self.stamps = [torch.zeros(n, dtype=torch.int32, device=self.device) for n in slots]
+        self.stamp = 0
+        self.counters = torch.zeros((self.T, 4), dtype=torch.int64, device=self.device)
+        self.stats = {"misses": 0, "writebacks": 0, "accesses": 0}
+        self._slots = None
+
+    # ------------------------------------------------------------------
+    def map_batch(self, indices: torch.Tensor, table_counts: Sequence[int], err: Optional[ErrorRecord] = None):
+        """Slot ids (int32, the layout of `indices`) of one batch; fetches and
+        writes back rows as needed.  Raises InvalidValue when a set needs more
+        than `ways` rows in one batch, IndexOutOfRange on a bad id."""
+        self.stamp += 1
+        n = int(indices.numel())
+        slots = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        own_err = err is None
+        err = err or ErrorRecord(self.device).reset()
+        off = np.concatenate(([0], np.cumsum(table_counts))).astype(np.int64)
+        isz = indices.element_size()
+        for t in range(self.T):
+            cnt = int(off[t + 1] - off[t])
+            if cnt == 0:
+                continue
+            ws = WORKSPACE.get("tier", capi.lib().neo_tier_workspace_bytes(cnt), self.device)
+            m = self.cache.moments[t]
+            rc = capi.lib().neo_tier_prepare(
+                self.rows[t], self.num_sets[t], self.ways, indices.data_ptr() + int(off[t]) * isz,
+                INDEX_CODE[indices.dtype], cnt, self.tags[t].data_ptr(), self.stamps[t].data_ptr(), self.stamp,
+                self.cache.weights[t].data_ptr(), None if m is None else m.data_ptr(), self.host_w[t].data_ptr(),
+                None if self.host_m[t] is None else self.host_m[t].data_ptr(), self.row_bytes[t], self.mom_bytes[t],
+                slots.data_ptr() + int(off[t]) * 4, self.counters[t].data_ptr(), ws.data_ptr(), ws.numel(),
+                err.ptr, _stream())
+            capi.check(rc, "neo_tier_prepare")
+        c = self.counters.cpu().numpy()
+        if own_err:
+            raise_if_bad(err, self.table_ids)
+        if c[:, 2].sum() > 0:
+            raise InvalidValue("num_sets", f"{int(c[:, 2].sum())} accesses found no free way: a set needs more than "
+                                           f"{self.ways} rows in one batch")
+        self.stats["misses"] += int(c[:, 0].sum())
+        self.stats["writebacks"] += int(c[:, 1].sum())
+        self.stats["accesses"] += n
+        self._slots = slots[:n]
+        return self._slots
+
+    def forward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, table_counts: Sequence[int],
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        slots = self.map_batch(indices, table_counts)
+        return self.cache.forward(slots, offsets, batch, out=out)
+
+    def backward(self, offsets: torch.Tensor, batch: int, grad: torch.Tensor, table_counts: Sequence[int],
+                 lr: float, eps: float, optim: Optional[str] = None) -> None:
+        """Fused backward + optimizer for the batch of the last forward()."""
+        if self._slots is None:
+            raise InvalidValue("backward", "no mapped batch: call forward() first")
+        self.cache.backward(self._slots, offsets, batch, grad, mode="update", optim=optim or self.optim, lr=lr,
+                            eps=eps, table_counts=table_counts)
+
+    def flush(self) -> None:
+        """Write every cached row (and its optimizer state) back to host memory."""
+        for t in range(self.T):
+            m = self.cache.moments[t]
+            rc = capi.lib().neo_tier_flush(self.tags[t].numel(), self.tags[t].data_ptr(),
+                                           self.cache.weights[t].data_ptr(), None if m is None else m.data_ptr(),
+                                           self.host_w[t].data_ptr(),
+                                           None if self.host_m[t] is None else self.host_m[t].data_ptr(),
+                                           self.row_bytes[t], self.mom_bytes[t], _stream())
+            capi.check(rc, "neo_tier_flush")
+        torch.cuda.current_stream(self.device).synchronize()

@@ -1,0 +1,93 @@
+"""GPU: training through the HBM tier over host-resident tables
+(tier.TieredTableGroup: pinned host rows + HBM slot cache + neo_tier_prepare)
+matches training the same tables fully in HBM: pooled outputs every step,
+and the flushed host tables and optimizer state after the last step.
+BITWISE on uniform ids; on skewed ids the backward folds hot rows through
+128-entry chunk partials whose grouping follows the row's position in the
+sorted stream (slot order vs row order), so there the bar is f32
+summation-order tolerance (1e-4 relative after several steps).  The cache holds a small fraction of the rows, so rows are
+evicted, written back and re-fetched across steps."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mods():
+    import paper_2104_05158_b200 as p
+    from paper_2104_05158_b200 import tbe, tier
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    p.load()
+    return tbe, tier
+
+
+@pytest.mark.parametrize("dtype,optim,zipf", [(torch.float32, "rowwise_adagrad", 0.0),
+                                              (torch.float32, "rowwise_adagrad", 1.1),
+                                              (torch.float16, "rowwise_adagrad", 0.0),
+                                              (torch.float32, "sgd", 1.05),
+                                              (torch.float32, "adagrad", 0.0)])
+def test_tier_training_matches_full_hbm(mods, dtype, optim, zipf):
+    tbe, tier = mods
+    rows, dims, B, L, steps = [60000, 20000], [128, 64], 512, 8, 4
+    T = len(rows)
+    rng = np.random.default_rng(17)
+    init = [rng.standard_normal((r, d)).astype(np.float32) for r, d in zip(rows, dims)]
+    full = tbe.TableGroup(rows, dims, dtype=dtype, optim=optim)
+    for w, v in zip(full.weights, init):
+        w.copy_(torch.from_numpy(v).to(dtype))
+    tg = tier.TieredTableGroup(rows, dims, num_sets=[512, 256], ways=32, dtype=dtype, optim=optim)
+    for t in range(T):
+        tg.host_w[t].copy_(torch.from_numpy(init[t]).to(dtype))
+    counts = [B * L] * T
+    off = torch.arange(0, T * B + 1, dtype=torch.int64, device="cuda") * L
+    for s in range(steps):
+        parts = []
+        for r in rows:
+            if zipf > 0:
+                parts.append(np.minimum(rng.zipf(zipf, B * L) - 1, r - 1))
+            else:
+                parts.append(rng.integers(0, r, B * L))
+        ix = torch.from_numpy(np.concatenate(parts).astype(np.int32)).cuda()
+        up = torch.from_numpy(rng.standard_normal((B, sum(dims))).astype(np.float32)).cuda()
+        a = full.forward(ix, off, B)
+        b = tg.forward(ix, off, B, counts)
+        if zipf == 0:
+            assert torch.equal(a, b), f"pooled outputs differ at step {s}"
+        else:
+            # the weights entering this forward already carry the summation-order
+            # differences of the previous steps' hot-row gradients
+            assert torch.allclose(a, b, rtol=1e-4, atol=1e-5 * float(a.abs().max())), f"pooled outputs, step {s}"
+        full.backward(ix, off, B, up, mode="update", optim=optim, lr=0.05, eps=1e-8, table_counts=counts)
+        tg.backward(off, B, up, counts, lr=0.05, eps=1e-8)
+    tg.flush()
+    assert tg.stats["misses"] > 0
+    if zipf == 0:
+        assert tg.stats["writebacks"] > 0  # uniform ids overflow the cache: rows were evicted and re-fetched
+    for t in range(T):
+        fw, hw = full.weights[t].cpu(), tg.host_w[t]
+        if zipf == 0:
+            assert torch.equal(fw, hw), f"table {t} values"
+        else:
+            assert torch.allclose(fw.float(), hw.float(), rtol=1e-4, atol=1e-5), f"table {t} values"
+        if full.moments[t] is not None:
+            fm, hm = full.moments[t].cpu(), tg.host_m[t]
+            if zipf == 0:
+                assert torch.equal(fm, hm), f"table {t} optimizer state"
+            else:
+                assert torch.allclose(fm, hm, rtol=1e-4, atol=1e-7), f"table {t} optimizer state"
+
+
+def test_tier_errors(mods):
+    tbe, tier = mods
+    tg = tier.TieredTableGroup([1000], [32], num_sets=1, ways=2)
+    off = torch.tensor([0, 4], dtype=torch.int64, device="cuda")
+    with pytest.raises(tier.InvalidValue):  # one set, 2 ways, 3 distinct rows in one batch
+        tg.forward(torch.tensor([1, 2, 3, 1], dtype=torch.int32, device="cuda"), off, 1, [4])
+    tg2 = tier.TieredTableGroup([1000], [32], num_sets=8, ways=4, table_ids=["emb"])
+    import paper_2104_05158_b200 as p
+
+    with pytest.raises(p.IndexOutOfRange):
+        tg2.forward(torch.tensor([1, 2, 1000, 1], dtype=torch.int32, device="cuda"), off, 1, [4])
