@@ -276,30 +276,48 @@ tier_assign_kernel(const Idx* __restrict__ ids, const int32_t* __restrict__ pos,
     const int64_t base = set_id * ways;
     int64_t tag = lane < ways ? tags[base + lane] : -2;
     uint32_t st = lane < ways ? stamps[base + lane] : 0xffffffffu;
-    // pass 1: stamp the ways this batch uses
+    // pass 1: stamp the ways this batch uses (lane-parallel: the 32 accesses
+    // of a window against each way's tag)
     for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
       const int mm = (int)min64(kWarp, s1 - j0);
       const int64_t my_r = lane < mm ? (int64_t)ids[pos[j0 + lane]] : -1;
-      for (int k = 0; k < mm; ++k) {
-        const int64_t r = __shfl_sync(full, my_r, k);
-        if (tag == r && r >= 0) st = stamp;
+      for (int w = 0; w < ways; ++w) {
+        const int64_t tw = __shfl_sync(full, tag, w);
+        if (__any_sync(full, tw >= 0 && my_r == tw) && lane == w) st = stamp;
       }
     }
-    // pass 2: map every access to its slot, filling misses
+    // pass 2: map every access to its slot, filling misses.  A run of accesses
+    // repeating the previous access's row (hot rows) shares its slot.
+    int64_t prev_r = -1;
+    int32_t prev_slot = -1;
     for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
       const int mm = (int)min64(kWarp, s1 - j0);
       const int32_t my_p = lane < mm ? pos[j0 + lane] : 0;
       const int64_t my_r = lane < mm ? (int64_t)ids[my_p] : -1;
-      for (int k = 0; k < mm; ++k) {
+      int64_t up = __shfl_up_sync(full, my_r, 1);
+      if (lane == 0) up = prev_r;
+      const unsigned same = __ballot_sync(full, lane < mm && my_r >= 0 && my_r < H && my_r == up);
+      for (int k = 0; k < mm;) {
+        if ((same >> k) & 1u) {
+          const unsigned rest = ~(same >> k);
+          const int L = min(rest ? __ffs(rest) - 1 : kWarp - k, mm - k);
+          if (lane >= k && lane < k + L) slots_out[my_p] = prev_slot;
+          k += L;
+          continue;
+        }
         const int64_t r = __shfl_sync(full, my_r, k);
         const int32_t p = __shfl_sync(full, my_p, k);
+        ++k;
+        prev_r = r;
+        prev_slot = -1;
         if (r < 0 || r >= H) {  // reported through err by the key kernel
           if (lane == 0) slots_out[p] = -1;
           continue;
         }
         const unsigned hm = __ballot_sync(full, tag == r);
         if (hm) {
-          if (lane == 0) slots_out[p] = (int32_t)(base + __ffs(hm) - 1);
+          prev_slot = (int32_t)(base + __ffs(hm) - 1);
+          if (lane == 0) slots_out[p] = prev_slot;
           continue;
         }
         const bool cand = lane < ways && st != stamp;
@@ -318,14 +336,16 @@ tier_assign_kernel(const Idx* __restrict__ ids, const int32_t* __restrict__ pos,
           tag = r;
           st = stamp;
         }
+        prev_slot = (int32_t)(base + v);
         if (lane == 0) {
           const unsigned long long x = atomicAdd(counters + 3, 1ull);
           xfer[3 * x + 0] = base + v;
           xfer[3 * x + 1] = old;
           xfer[3 * x + 2] = r;
-          slots_out[p] = (int32_t)(base + v);
+          slots_out[p] = prev_slot;
         }
       }
+      prev_r = __shfl_sync(full, my_r, mm - 1);
     }
     if (lane < ways) {
       tags[base + lane] = tag;
