@@ -10,8 +10,11 @@ HBM as an ordinary ``TableGroup``, and every batch is mapped onto slots by
 ``neo_tier_prepare`` (csrc/cache.cu) before the unchanged TBE forward and
 fused backward run on the slots.  Evicted rows (values + moments) are written
 back, missing rows fetched, in the same stream.  Rows a batch uses are never
-evicted by it, so results are bitwise identical to training with the whole
-table in HBM (tests/test_gpu_tier.py).
+evicted by it, so the same rows feed the same kernels as with the whole table
+in HBM: results are bitwise identical on uniform ids, and within f32
+summation order where hot rows are folded through 128-entry chunk partials
+(their grouping follows slot order instead of row order;
+tests/test_gpu_tier.py).
 """
 from __future__ import annotations
 
