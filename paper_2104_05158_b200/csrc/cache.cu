@@ -380,6 +380,42 @@ tier_transfer_kernel(const int64_t* __restrict__ xfer, const unsigned long long*
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / kWarp;
   const int64_t nx = (int64_t)counters[3];
+  constexpr int U = 4;  // transfers per warp step: U host rows in flight per lane
+  const bool fast = row_bytes <= 16 * kWarp && (row_bytes & 15) == 0 && (mom_bytes == 0 || mom_bytes == 4) &&
+                    aligned16(cache_w) && aligned16(host_w);
+  if (fast) {
+    const bool act = lane * 16 < row_bytes;
+    for (int64_t i0 = warp * U; i0 < nx; i0 += nwarps * U) {
+      int64_t slot[U], old[U], r[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = i0 + u < nx;
+        slot[u] = ok ? xfer[3 * (i0 + u)] : -1;
+        old[u] = ok ? xfer[3 * (i0 + u) + 1] : -1;
+        r[u] = ok ? xfer[3 * (i0 + u) + 2] : -1;
+      }
+      uint4 v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)  // write back the evicted rows (HBM -> host)
+        if (act && old[u] >= 0) v[u] = *reinterpret_cast<const uint4*>(cache_w + slot[u] * row_bytes + lane * 16);
+      float mv = 0.f;
+      if (mom_bytes && lane < U && old[lane] >= 0)
+        mv = *reinterpret_cast<const float*>(cache_m + slot[lane] * 4);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (act && old[u] >= 0) *reinterpret_cast<uint4*>(host_w + old[u] * row_bytes + lane * 16) = v[u];
+      if (mom_bytes && lane < U && old[lane] >= 0) *reinterpret_cast<float*>(host_m + old[lane] * 4) = mv;
+#pragma unroll
+      for (int u = 0; u < U; ++u)  // fetch (host -> HBM): U loads in flight per lane
+        if (act && r[u] >= 0) v[u] = *reinterpret_cast<const uint4*>(host_w + r[u] * row_bytes + lane * 16);
+      if (mom_bytes && lane < U && r[lane] >= 0) mv = *reinterpret_cast<const float*>(host_m + r[lane] * 4);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (act && r[u] >= 0) *reinterpret_cast<uint4*>(cache_w + slot[u] * row_bytes + lane * 16) = v[u];
+      if (mom_bytes && lane < U && r[lane] >= 0) *reinterpret_cast<float*>(cache_m + slot[lane] * 4) = mv;
+    }
+    return;
+  }
   for (int64_t i = warp; i < nx; i += nwarps) {
     const int64_t slot = xfer[3 * i], old = xfer[3 * i + 1], r = xfer[3 * i + 2];
     if (old >= 0) {  // write back the evicted row and its optimizer state
