@@ -363,7 +363,7 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
             (reinterpret_cast<uintptr_t>(grad) % min(16, (int)(sizeof(G) * kVec))) == 0;
     w.gofs = (uint32_t)(((int64_t)bag - (int64_t)t * p.B) * p.grad_stride + doff);
     w.wptr = reinterpret_cast<uint64_t>(wbase + row * D);
-    if (OPT != NEO_OPT_SGD) {
+    if (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD) {
       float* mb = reinterpret_cast<float*>(p.moments[t]);
       w.mptr = reinterpret_cast<uint64_t>(OPT == NEO_OPT_ROWWISE_ADAGRAD ? mb + row : mb + row * D);
     }
@@ -829,6 +829,28 @@ static int launch_stream(const SegParams& p, cudaStream_t s) {
   }
 }
 
+// DENSE mode on the pipelined walk (f32 tables): each touched row's
+// aggregated gradient is stored into dense_grads[t] (passed as the "weights")
+template <typename G, typename Key>
+static int launch_dense_pipe(SegParams p, cudaStream_t s) {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  p.weights = p.dense_grads;
+  p.moments = nullptr;
+  if (cudaMemsetAsync(p.chunk_counter, 0, 2 * sizeof(int64_t), s) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tbe_backward: counter reset failed");
+  const int64_t chunks = (p.N + kChunk - 1) / kChunk;
+  const int64_t hb = (chunks + 7) / 8;
+  const unsigned hgrid = (unsigned)(hb < (int64_t)sms * 16 ? (hb > 0 ? hb : 1) : (int64_t)sms * 16);
+  const bool wide = p.max_dim > kWarp * 4;
+  if (wide) hot_chunk_kernel<float, G, Key, 2><<<hgrid, 256, 0, s>>>(p);
+  else hot_chunk_kernel<float, G, Key, 1><<<hgrid, 256, 0, s>>>(p);
+  const int rc = check_launch("neo_tbe_backward(hot chunks)");
+  if (rc) return rc;
+  return wide ? launch_pipe<float, G, Key, NEO_OPT_NONE, 2>(p, s, sms) : launch_pipe<float, G, Key, NEO_OPT_NONE, 1>(p, s, sms);
+}
+
 template <typename Key>
 __global__ void count_valid_kernel(const Key* keys, const int32_t* seg_starts,
                                    const int64_t* num_segs, int64_t total_rows, int64_t* out) {
@@ -931,6 +953,9 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   const bool fast = weight_dtype != NEO_F64 && p.mode == NEO_BWD_UPDATE && p.pooling == NEO_POOL_SUM &&
                     p.max_dim <= 2 * kWarp * wvec && !out_count &&
                     p.B * p.grad_stride < (int64_t(1) << 32);  // 32-bit upstream offsets
+  const bool dense_fast = weight_dtype == NEO_F32 && p.mode == NEO_BWD_DENSE && p.pooling == NEO_POOL_SUM &&
+                          (p.flags & NEO_BWD_FLAG_ALIGNED) && p.max_dim <= 2 * kWarp * 4 && !out_count &&
+                          p.B * p.grad_stride < (int64_t(1) << 32) && use_pipe_variant();
   if ((prepare_only || apply_only) && !fast)
     return fail(NEO_E_ARG, "neo_tbe_backward: PREPARE/APPLY need the streamed UPDATE path");
   int rc = NEO_OK;
@@ -971,6 +996,17 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
   p.bags = vbuf.Current();
   p.chunk_counter = nseg + 1;
   p.pool_counter = reinterpret_cast<unsigned*>(nseg + 2);
+  if (dense_fast) {
+    switch (grad_dtype) {
+      case NEO_F32: rc = launch_dense_pipe<float, Key>(p, s); break;
+      case NEO_BF16: rc = launch_dense_pipe<__nv_bfloat16, Key>(p, s); break;
+      case NEO_F16: rc = launch_dense_pipe<__half, Key>(p, s); break;
+      default: return fail(NEO_E_ARG, "neo_tbe_backward: gradient dtype must be F32, BF16 or F16");
+    }
+    if (rc) return rc;
+    launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
+    return check_launch("neo_tbe_backward(finalize)");
+  }
   if (fast) {
     const bool h = weight_dtype == NEO_F16;
     switch (grad_dtype) {

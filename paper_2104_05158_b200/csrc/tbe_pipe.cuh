@@ -203,10 +203,12 @@ tbe_pipe_update_kernel(SegParams p) {
         const W* wrow = reinterpret_cast<const W*>(__shfl_sync(full, w.wptr, l + e));
         int De = 0;
         if (!FULL) De = __shfl_sync(full, w.D, l + e);
+        if (OPT != NEO_OPT_NONE) {  // DENSE mode (OPT_NONE) only writes the row
 #pragma unroll
-        for (int v = 0; v < VPL; ++v)
-          if (FULL || (lane + v * kWarp) * kVec < De)
-            cp_async(st + C::kWOff + ((e * VPL + v) * kWarp + lane) * 16, wrow + (lane + v * kWarp) * kVec, 16);
+          for (int v = 0; v < VPL; ++v)
+            if (FULL || (lane + v * kWarp) * kVec < De)
+              cp_async(st + C::kWOff + ((e * VPL + v) * kWarp + lane) * 16, wrow + (lane + v * kWarp) * kVec, 16);
+        }
         if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
           const uint64_t mp = __shfl_sync(full, w.mptr, l + e);
           if (lane == 0) cp_async(st + C::kRowMOff + e * 4, reinterpret_cast<const float*>(mp), 4);
@@ -299,6 +301,19 @@ tbe_pipe_update_kernel(SegParams p) {
   auto live_at = [&](int v) -> bool { return FULL || (lane + v * kWarp) * kVec < cD; };
 
   auto finalize = [&]() {  // exactly one optimizer step for the open row
+    if (OPT == NEO_OPT_NONE) {  // DENSE mode: the aggregated gradient row itself
+      float* drow = reinterpret_cast<float*>(cw);
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        if (live_at(v))
+#pragma unroll
+          for (int e = 0; e < kVec; e += 4)
+            *reinterpret_cast<float4*>(drow + (lane + v * kWarp) * kVec + e) =
+                make_float4(acc[v * kVec + e], acc[v * kVec + e + 1], acc[v * kVec + e + 2], acc[v * kVec + e + 3]);
+#pragma unroll
+      for (int e = 0; e < VPL * kVec; ++e) acc[e] = 0.f;
+      return;
+    }
     if (!FULL) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v)
@@ -433,9 +448,11 @@ tbe_pipe_update_kernel(SegParams p) {
           if ((heads >> e) & 1u) {
             if (open) finalize();
             open = true;
+            if (OPT != NEO_OPT_NONE) {
 #pragma unroll
-            for (int v = 0; v < VPL; ++v)
-              wr[v] = *reinterpret_cast<const uint4*>(st + C::kWOff + ((e * VPL + v) * kWarp + lane) * 16);
+              for (int v = 0; v < VPL; ++v)
+                wr[v] = *reinterpret_cast<const uint4*>(st + C::kWOff + ((e * VPL + v) * kWarp + lane) * 16);
+            }
             if (OPT == NEO_OPT_ROWWISE_ADAGRAD) mrow = *reinterpret_cast<const float*>(st + C::kRowMOff + e * 4);
             if (OPT == NEO_OPT_ADAGRAD) {
 #pragma unroll

@@ -206,11 +206,12 @@ class TableGroup:
             dense_ptrs = _u64_ptrs(dense_grads, self.device)
         optim = optim or self.optim or "sgd"
         stride = grad.stride(0) if grad.dim() == 2 else self.total_dim
-        if mode == "update":  # layout promises that select the specialised fast path
+        if mode in ("update", "dense"):  # layout promises that select the specialised fast paths
             vec = 16 // torch.empty(0, dtype=self.dtype).element_size()
             aligned = (all(d % vec == 0 for d in self.dims) and stride % vec == 0
                        and grad.data_ptr() % 16 == 0
-                       and all(w is None or w.data_ptr() % 16 == 0 for w in self.weights))
+                       and all(w is None or w.data_ptr() % 16 == 0 for w in self.weights)
+                       and (mode != "dense" or all(g.data_ptr() % 16 == 0 for g in dense_grads)))
             if aligned:
                 mode_code |= capi.NEO_BWD_FLAG_ALIGNED
                 if all(d == 32 * vec for d in self.dims):

@@ -136,3 +136,43 @@ def test_prepare_backward_on_side_stream_matches(tbe):
         outs.append((pooled.clone(), grp._storage.clone(), torch.cat([m.flatten() for m in grp.moments])))
     for a, b in zip(outs[0], outs[1]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("zipf", [0.0, 1.1])
+def test_dense_mode_pipe_matches_oracle(tbe, zipf):
+    """mode="dense" (the data-parallel tables' gradient) on the pipelined walk
+    and on the warp-per-segment kernel (NEO_BWD_VARIANT=stream routes dense
+    there) against the f64 oracle aggregate: |got - ref| <= 1e-5 * sum|terms|."""
+    rows, dims, B = [30000, 8000, 12000], [128, 64, 256], 2048
+    T = len(rows)
+    rng = np.random.default_rng(21)
+    lengths = rng.integers(0, 40, size=(T, B))
+    parts = []
+    for t in range(T):
+        n = int(lengths[t].sum())
+        parts.append(np.minimum(rng.zipf(zipf, n) - 1, rows[t] - 1) if zipf else rng.integers(0, rows[t], n))
+    idx = np.concatenate(parts)
+    ix = torch.from_numpy(idx.astype(np.int32)).cuda()
+    off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+    up_np = rng.standard_normal((B, sum(dims))).astype(np.float32)
+    up = torch.from_numpy(up_np).cuda()
+    counts = [int(c) for c in lengths.sum(axis=1)]
+    grp = tbe.TableGroup(rows, dims, dtype=torch.float32, optim="sgd")
+    tab_off = O.offsets_of(lengths.sum(axis=1))
+    for variant in ("stream", "pipe"):
+        dense = [torch.zeros((r, d), dtype=torch.float32, device="cuda") for r, d in zip(rows, dims)]
+        os.environ["NEO_BWD_VARIANT"] = variant
+        try:
+            grp.backward(ix, off, B, up, mode="dense", dense_grads=dense, table_counts=counts)
+            torch.cuda.synchronize()
+        finally:
+            os.environ.pop("NEO_BWD_VARIANT", None)
+        col = 0
+        for t, D in enumerate(dims):
+            part = idx[tab_off[t]:tab_off[t + 1]]
+            u = np.ascontiguousarray(up_np[:, col:col + D].astype(np.float64))
+            ids, gr = O.backward_aggregate_c(lengths[t], part, u)
+            _, ga = O.backward_aggregate_c(lengths[t], part, np.abs(u))
+            got = dense[t].double().cpu().numpy()[ids]
+            assert (np.abs(got - gr) <= 1e-5 * ga + 1e-30).all(), f"{variant}: table {t}"
+            col += D
