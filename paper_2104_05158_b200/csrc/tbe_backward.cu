@@ -60,25 +60,37 @@ build_keys_kernel(int32_t T, int64_t B, const int64_t* __restrict__ row_offsets,
                   const Idx* __restrict__ indices, const int64_t* __restrict__ offsets,
                   Key* __restrict__ keys, int32_t* __restrict__ bags, Key sentinel,
                   neo_error* err) {
+  // persistent warps, 4 consecutive bags per step: their ids form one
+  // contiguous range walked with independent (coalesced) loads
+  constexpr int kBags = 4;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  const int64_t bag = (int64_t)blockIdx.x * 8 + warp;
-  if (bag >= (int64_t)T * B) return;
-  const int32_t t = (int32_t)(bag / B);
-  const int64_t rbase = row_offsets[t];
-  const int64_t H = row_offsets[t + 1] - rbase;
+  const int64_t nb = (int64_t)T * B;
   const int64_t base0 = offsets[0];
-  const int64_t start = offsets[bag], end = offsets[bag + 1];
-  for (int64_t p = start + lane; p < end; p += kWarp) {
-    const int64_t v = (int64_t)indices[p];
-    Key k;
-    if (v < 0 || v >= H) {
-      record_bad_index(err, p);
-      k = sentinel;
-    } else {
-      k = (Key)(rbase + v);
+  for (int64_t b0 = ((int64_t)blockIdx.x * 8 + warp) * kBags; b0 < nb; b0 += (int64_t)gridDim.x * 8 * kBags) {
+    const int n = (int)min64(kBags, nb - b0);
+    const int64_t o = lane <= n ? offsets[b0 + lane] : 0;
+    const int64_t start = __shfl_sync(0xffffffffu, o, 0), end = __shfl_sync(0xffffffffu, o, n);
+    const int64_t o1 = n > 1 ? __shfl_sync(0xffffffffu, o, 1) : end;
+    const int64_t o2 = n > 2 ? __shfl_sync(0xffffffffu, o, 2) : end;
+    const int64_t o3 = n > 3 ? __shfl_sync(0xffffffffu, o, 3) : end;
+    const int32_t t0 = (int32_t)(b0 / B);
+    for (int64_t p = start + lane; p < end; p += kWarp) {
+      const int64_t bag = b0 + (p >= o1) + (p >= o2) + (p >= o3);
+      int32_t t = t0;
+      while (bag >= (int64_t)(t + 1) * B) ++t;
+      const int64_t rbase = row_offsets[t];
+      const int64_t H = row_offsets[t + 1] - rbase;
+      const int64_t v = (int64_t)indices[p];
+      Key k;
+      if (v < 0 || v >= H) {
+        record_bad_index(err, p);
+        k = sentinel;
+      } else {
+        k = (Key)(rbase + v);
+      }
+      keys[p - base0] = k;
+      bags[p - base0] = (int32_t)bag;
     }
-    keys[p - base0] = k;
-    bags[p - base0] = (int32_t)bag;
   }
 }
 
@@ -969,7 +981,11 @@ static int run_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype,
     g_prep_sel.erase(it);
   } else {
   const int64_t bags = (int64_t)p.T * p.B;
-  const unsigned kb_blocks = (unsigned)((bags + 7) / 8);
+  int kb_dev = 0, kb_sms = 0;
+  cudaGetDevice(&kb_dev);
+  cudaDeviceGetAttribute(&kb_sms, cudaDevAttrMultiProcessorCount, kb_dev);
+  const int64_t kb_want = (bags + 8 * 4 - 1) / (8 * 4);
+  const unsigned kb_blocks = (unsigned)(kb_want < (int64_t)kb_sms * 8 ? (kb_want > 0 ? kb_want : 1) : (int64_t)kb_sms * 8);
   const Key sentinel = (Key)p.total_rows;
   if (index_dtype == NEO_I32)
     build_keys_kernel<int32_t, Key><<<kb_blocks, 256, 0, s>>>(
