@@ -30,6 +30,7 @@
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
+#include <cuda.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -137,6 +138,7 @@ struct SegParams {
   float* pool;             // partial sums of such chunks (slot x max_dim, f32)
   unsigned* pool_counter;
   int64_t pool_cap;
+  int32_t tma;             // pipelined walk: upstream rows staged by TMA gather4 (uniform full rows)
 };
 
 // aggregate the segment's upstream rows into g (warp-private smem row)
@@ -341,6 +343,9 @@ struct Window {
   uint64_t mptr;    // moment (row-wise scalar / element-wise row)
   int32_t D;        // table dim of this lane's entry
   int32_t vec;      // 16-byte vector path usable for this entry's table
+  int32_t tt;       // table of this lane's entry (-1: invalid)
+  uint32_t grow;    // upstream row (bag within the table)
+  int32_t dcol;     // upstream column offset of the table
 };
 
 template <typename W, typename G, typename Key, int OPT>
@@ -363,8 +368,14 @@ __device__ __forceinline__ void load_window(const SegParams& p, int64_t base, ui
   w.wptr = w.mptr = 0;
   w.D = 0;
   w.vec = 0;
+  w.tt = -1;
+  w.grow = 0;
+  w.dcol = 0;
   if (ok) {
     const int32_t t = bag / (int32_t)p.B;
+    w.tt = t;
+    w.grow = (uint32_t)(bag - t * (int32_t)p.B);
+    w.dcol = p.dim_offsets[t];
     const int64_t row = (int64_t)w.key - p.row_offsets[t];
     const int32_t doff = p.dim_offsets[t];
     const int32_t D = p.dim_offsets[t + 1] - doff;
@@ -771,9 +782,50 @@ static bool use_pipe_variant() {
   return !(v && std::strcmp(v, "stream") == 0);
 }
 
+typedef CUresult (*TensorMapEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2D map over the upstream gradient (B rows x grad_stride columns), box = one
+// row of `cols` elements: gather4 then stages four upstream rows per instruction
+template <typename G>
+static bool encode_upstream_map(const SegParams& p, int cols, CUtensorMap* map) {
+  static TensorMapEncodeFn enc = [] {
+    TensorMapEncodeFn f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (TensorMapEncodeFn) nullptr;
+    return f;
+  }();
+  if (!enc || cols > 256 || (reinterpret_cast<uintptr_t>(p.grad) & 15) || ((p.grad_stride * sizeof(G)) & 15))
+    return false;
+  const CUtensorMapDataType dt = sizeof(G) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : std::is_same<G, __half>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                                  : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  cuuint64_t dims[2] = {(cuuint64_t)p.grad_stride, (cuuint64_t)p.B};
+  cuuint64_t strides[1] = {(cuuint64_t)p.grad_stride * sizeof(G)};
+  cuuint32_t box[2] = {(cuuint32_t)cols, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, dt, 2, const_cast<void*>(p.grad), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
+static bool use_pipe_tma() {
+  const char* v = std::getenv("NEO_PIPE_TMA");
+  return v && std::strcmp(v, "1") == 0;
+}
+
 template <typename W, typename G, typename Key, int OPT, int VPL>
-static int launch_pipe(const SegParams& p, cudaStream_t s, int sms) {
+static int launch_pipe(SegParams p, cudaStream_t s, int sms) {
   using Cfg = PipeCfg<W, G, OPT, VPL>;
+  CUtensorMap gmap;
+  std::memset(&gmap, 0, sizeof(gmap));
+  p.tma = 0;
+  if ((p.flags & NEO_BWD_FLAG_FULL_ROWS) && use_pipe_tma() &&
+      encode_upstream_map<G>(p, kWarp * Cfg::kVec * VPL, &gmap))
+    p.tma = 1;
   auto kern = tbe_pipe_update_kernel<W, G, Key, OPT, false, VPL>;
   if (p.flags & NEO_BWD_FLAG_FULL_ROWS) kern = tbe_pipe_update_kernel<W, G, Key, OPT, true, VPL>;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem) != cudaSuccess)
@@ -785,7 +837,7 @@ static int launch_pipe(const SegParams& p, cudaStream_t s, int sms) {
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > (tasks + Cfg::P - 1) / Cfg::P) grid = (tasks + Cfg::P - 1) / Cfg::P;
   if (grid < 1) grid = 1;
-  kern<<<(unsigned)grid, 2 * Cfg::P * kWarp, Cfg::kSmem, s>>>(p);
+  kern<<<(unsigned)grid, 2 * Cfg::P * kWarp, Cfg::kSmem, s>>>(p, gmap);
   return check_launch("neo_tbe_backward(pipe)");
 }
 

@@ -118,7 +118,7 @@ struct PipeCfg {
 
 template <typename W, typename G, typename Key, int OPT, bool FULL, int VPL>
 __global__ void __launch_bounds__(2 * PipeCfg<W, G, OPT, VPL>::P * kWarp, NEO_PIPE_MINB)
-tbe_pipe_update_kernel(SegParams p) {
+tbe_pipe_update_kernel(SegParams p, const __grid_constant__ CUtensorMap gmap) {
   using C = PipeCfg<W, G, OPT, VPL>;
   using Meta = typename C::Meta;
   constexpr int kVec = C::kVec, kGB = C::kGB, E = C::E, S = C::S, P = C::P;
@@ -180,8 +180,32 @@ tbe_pipe_update_kernel(SegParams p) {
         m.flags = 0;
       }
       unsigned char* gs = st + C::kGOff;
+      bool staged = false;
+      if (FULL && p.tma) {
+        // one gather4 stages the stage's rows when they come from one table
+        const int32_t my_t = (lane >= l && lane < l + n) ? w.tt : -1;
+        const int32_t t0 = __shfl_sync(full, w.tt, l);
+        if (n == E && E == 4 && __all_sync(full, my_t == -1 || my_t == t0)) {
+          const int32_t dcol0 = __shfl_sync(full, w.dcol, l);
+          uint32_t r[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) r[q] = (uint32_t)__shfl_sync(full, w.grow, l + q);
+          if (lane == 0) {
+            // expect the bytes before the copy is issued; the plain arrive in publish() follows
+            asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(bars + s * 16),
+                         "r"(4u * (uint32_t)(kWarp * kGB * VPL))
+                         : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                "%3, %4, %5, %6}], [%7];\n" ::"r"(smem_u32(gs)),
+                "l"(&gmap), "r"(dcol0), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(bars + s * 16)
+                : "memory");
+          }
+          staged = true;
+        }
+      }
 #pragma unroll 4
-      for (int e = 0; e < n; ++e) {
+      for (int e = 0; e < (staged ? 0 : n); ++e) {
         const G* grow = gbase + __shfl_sync(full, w.gofs, l + e);
         int De = 0;
         if (!FULL) De = __shfl_sync(full, w.D, l + e);

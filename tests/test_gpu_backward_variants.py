@@ -176,3 +176,18 @@ def test_dense_mode_pipe_matches_oracle(tbe, zipf):
             got = dense[t].double().cpu().numpy()[ids]
             assert (np.abs(got - gr) <= 1e-5 * ga + 1e-30).all(), f"{variant}: table {t}"
             col += D
+
+
+def test_tma_gather4_producer_bitwise(tbe):
+    """NEO_PIPE_TMA=1: the producer stages full 4-entry stages of upstream rows
+    with one TMA tile::gather4 each; results stay bitwise equal to the walk."""
+    old = os.environ.get("NEO_PIPE_TMA")
+    os.environ["NEO_PIPE_TMA"] = "1"
+    try:
+        for case in (0, 3):
+            test_pipe_matches_stream_bitwise_and_oracle(tbe, case)
+    finally:
+        if old is None:
+            os.environ.pop("NEO_PIPE_TMA", None)
+        else:
+            os.environ["NEO_PIPE_TMA"] = old
