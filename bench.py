@@ -593,6 +593,11 @@ def run_sharded(a, rank, world, dev):
 
     from paper_2104_05158_b200 import dist as nd
 
+    # stdout carries exactly one JSON line: anything the communicator setup
+    # prints (NCCL's version banner) is sent to stderr
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     tdist.init_process_group("nccl", device_id=dev)
     wl = ShardedWorkload(a, world)
     B = wl.B
@@ -602,7 +607,7 @@ def run_sharded(a, rank, world, dev):
         if rank == 0:
             print(json.dumps({"metric": METRIC, "unavailable": f"{a.workload} at {world} GPUs needs "
                               f"{need / 1e9:.0f} GB of tables per GPU (> 75% of {have / 1e9:.0f} GB); "
-                              "run it on more GPUs"}), flush=True)
+                              "run it on more GPUs"}), file=json_out, flush=True)
         tdist.destroy_process_group()
         return
     comm = nd.NcclComm()
@@ -700,7 +705,7 @@ def run_sharded(a, rank, world, dev):
                                            "(the transport the step uses), max over ranks"}
     if e2e is not None:
         line["e2e"] = e2e
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=json_out, flush=True)
     tdist.destroy_process_group()
 
 
