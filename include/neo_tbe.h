@@ -80,6 +80,13 @@ enum { NEO_BWD_FLAG_ALIGNED = 0x100, NEO_BWD_FLAG_FULL_ROWS = 0x200 };
  * ordered before it) runs the segment walk + optimizer.  Lets the sort of
  * one table group overlap the update of another. */
 enum { NEO_BWD_FLAG_PREPARE = 0x400, NEO_BWD_FLAG_APPLY = 0x800 };
+/* DIM8: every table's D is a multiple of 8 elements, the weight rows, the
+ * gradient base and its row stride are 16-byte aligned.  With SUM pooling,
+ * f32/f16 tables, UPDATE (or DENSE on f32) and D <= 256 this selects the
+ * bucketed backward (hand-written stable two-level counting sort by row +
+ * fused sub-warp-per-row reduce/optimizer); its workspace size is
+ * neo_tbe_bucket_workspace_bytes. */
+enum { NEO_BWD_FLAG_DIM8 = 0x1000 };
 
 /* Device-side error record (caller allocates sizeof(neo_error) bytes of
  * device memory).  position = first offending position in index-buffer
@@ -157,6 +164,9 @@ int neo_tbe_forward_scatter(int32_t num_tables, int64_t batch,
  * num_indices must equal offsets[T*B] - offsets[0] (the ids the bags cover).
  * Workspace size: neo_tbe_backward_workspace_bytes. */
 size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows, int32_t max_dim);
+/* workspace of the bucketed path (NEO_BWD_FLAG_DIM8) for T tables of B bags */
+size_t neo_tbe_bucket_workspace_bytes(int32_t num_tables, int64_t batch, int64_t num_indices,
+                                      int64_t total_rows);
 
 int neo_tbe_backward(int32_t num_tables, int64_t batch,
                      const int64_t* row_offsets, int64_t total_rows,

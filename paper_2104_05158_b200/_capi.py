@@ -22,6 +22,7 @@ NEO_OPT_SGD, NEO_OPT_ROWWISE_ADAGRAD, NEO_OPT_ADAGRAD, NEO_OPT_NONE = 0, 1, 2, 3
 NEO_BWD_UPDATE, NEO_BWD_AGGREGATE, NEO_BWD_DENSE = 0, 1, 2
 NEO_BWD_FLAG_ALIGNED, NEO_BWD_FLAG_FULL_ROWS = 0x100, 0x200
 NEO_BWD_FLAG_PREPARE, NEO_BWD_FLAG_APPLY = 0x400, 0x800
+NEO_BWD_FLAG_DIM8 = 0x1000
 NEO_CACHE_LRU, NEO_CACHE_LFU = 0, 1
 
 P = C.c_void_p
@@ -68,6 +69,7 @@ SIGNATURES = {
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I64, I32, I64, P, P],
     ),
     "neo_tbe_backward_workspace_bytes": (SZ, [I64, I64, I32]),
+    "neo_tbe_bucket_workspace_bytes": (SZ, [I32, I64, I64, I64]),
     "neo_tbe_backward": (
         C.c_int,
         [I32, I64, P, I64, P, I32, P, I32, P, P, I32, P, I64, I32, P, I32, I64,

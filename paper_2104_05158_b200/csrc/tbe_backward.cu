@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 #include <unordered_map>
 #include <cuda.h>
 #include <cub/device/device_radix_sort.cuh>
@@ -37,13 +38,13 @@
 
 #include "common.cuh"
 #include "optim.cuh"
+#include "bwd_common.cuh"
 
 namespace neo {
 
 constexpr int kBwdWarps = 8;
 constexpr int kBwdUnroll = 8;
 
-static inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 static inline int key_bits_for(int64_t total_rows) {
   // sentinel key == total_rows marks an invalid id; it must be representable
@@ -107,39 +108,7 @@ struct HeadFlag {
 // ---------------------------------------------------------------------------
 // 4. segment reduce + optimizer
 
-struct SegParams {
-  int32_t T;
-  int64_t B;
-  const int64_t* row_offsets;
-  int64_t total_rows;
-  const int32_t* dim_offsets;
-  int32_t max_dim;
-  const uint64_t* weights;
-  const uint64_t* moments;
-  const void* grad;
-  int64_t grad_stride;
-  int32_t pooling;
-  const int64_t* offsets;  // for MEAN pooling: bag lengths
-  int32_t mode;
-  int32_t optim;
-  double lr;
-  double eps;
-  int64_t* out_ids;
-  void* out_grads;
-  const uint64_t* dense_grads;
-  const void* keys;
-  const int32_t* bags;
-  const int32_t* seg_starts;
-  const int64_t* num_segs;
-  int64_t N;
-  int32_t flags;   // NEO_BWD_FLAG_* layout promises from the caller
-  int64_t* chunk_counter;  // work-queue counter of the streamed kernel (zeroed per launch)
-  int32_t* chunk_slot;     // per 128-entry chunk: partial-sum slot if the chunk lies inside one row, else -1
-  float* pool;             // partial sums of such chunks (slot x max_dim, f32)
-  unsigned* pool_counter;
-  int64_t pool_cap;
-  int32_t tma;             // pipelined walk: upstream rows staged by TMA gather4 (uniform full rows)
-};
+
 
 // aggregate the segment's upstream rows into g (warp-private smem row)
 template <typename G, typename Acc, int VEC>
@@ -1209,6 +1178,8 @@ extern "C" int neo_tbe_backward(int32_t num_tables, int64_t batch, const int64_t
   p.out_grads = out_grads;
   p.dense_grads = dense_grads;
   p.N = num_indices;
+  if (bkt_eligible(p, weight_dtype, grad_dtype, out_count != nullptr))
+    return run_bucket_backward(p, weight_dtype, grad_dtype, indices, index_dtype, workspace, workspace_bytes, err, s);
   if (use_wide_keys(total_rows))
     return run_backward<uint64_t>(p, weight_dtype, grad_dtype, indices, index_dtype, workspace,
                                   workspace_bytes, out_count, err, s);

@@ -12,6 +12,7 @@ current torch stream and never synchronise, except ``ErrorRecord.read``.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional, Sequence
 
@@ -216,6 +217,22 @@ class TableGroup:
                 mode_code |= capi.NEO_BWD_FLAG_ALIGNED
                 if all(d == 32 * vec for d in self.dims):
                     mode_code |= capi.NEO_BWD_FLAG_FULL_ROWS
+        if self._bucketed(mode, batch, grad, stride, pooling, dense_grads):
+            # hand-written bucketed sort + fused reduce/optimizer over the whole group
+            self._prepared = None
+            mode_code |= capi.NEO_BWD_FLAG_DIM8
+            n_b = n_idx if table_counts is None else int(sum(table_counts))
+            wsb = capi.lib().neo_tbe_bucket_workspace_bytes(self.T, batch, max(n_b, 1), self.total_rows)
+            ws = WORKSPACE.get("tbe_bucket", wsb, self.device)
+            if timers is not None:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling, err, 0,
+                                self.T, None, None, None, None, dense_ptrs, n_b, ws=ws)
+            if timers is not None:
+                e1.record()
+                timers.setdefault("apply", []).append((e0, e1, 0, self.T))
+            return None
         prep = getattr(self, "_prepared", None)
         if (mode == "update" and prep is not None and prep["key"] == (indices.data_ptr(), offsets.data_ptr(), batch)
                 and table_counts is not None):
@@ -243,6 +260,30 @@ class TableGroup:
             return out_ids, out_grads, out_count
         return None
 
+    def _bucketed(self, mode: str, batch: int, grad: torch.Tensor, stride: int, pooling: str,
+                  dense_grads=None) -> bool:
+        """Mirror of the C side's bucketed-path condition (bkt_eligible):
+        f32/f16 tables (f32 for DENSE), SUM, every D a multiple of 8 and
+        <= 256, 16-byte aligned rows and gradient."""
+        if os.environ.get("NEO_BWD_VARIANT") in ("pipe", "stream"):
+            return False
+        if pooling != "sum" or mode not in ("update", "dense") or self.max_dim > 256 or self.T == 0:
+            return False
+        if self.dtype not in (torch.float32, torch.float16) or (mode == "dense" and self.dtype != torch.float32):
+            return False
+        if grad.dtype not in (torch.float32, torch.bfloat16, torch.float16):
+            return False
+        if any(d % 8 for d in self.dims) or stride % 8 or grad.data_ptr() % 16:
+            return False
+        if any(w is not None and w.data_ptr() % 16 for w in self.weights):
+            return False
+        if mode == "dense" and any(g.data_ptr() % 16 for g in dense_grads):
+            return False
+        s = 4
+        while (self.total_rows + (1 << s) - 1) >> s > 2048:
+            s += 1
+        return s + max(1, (batch - 1).bit_length()) <= 32
+
     def prepare_backward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int, grad: torch.Tensor,
                          table_counts: Sequence[int], optim: Optional[str] = None, pooling: str = "sum",
                          err: Optional[ErrorRecord] = None) -> bool:
@@ -258,6 +299,8 @@ class TableGroup:
         stride = grad.stride(0) if grad.dim() == 2 else self.total_dim
         if not self._streamed(batch, stride, pooling) or self.total_rows < 1:
             return False
+        if self._bucketed("update", batch, grad, stride, pooling):
+            return False  # the bucketed backward has no separate sort phase
         groups = self._sort_groups() if self.total_rows >= (1 << SORT_BITS) else [(0, self.T)]
         if len(groups) == 1 and not hasattr(self, "_group_meta"):
             self._group_meta = {}
