@@ -22,20 +22,23 @@
 //                     in buffer order and places (row_low, bag) entries with
 //                     __match_any_sync ranking: a STABLE scatter, so every
 //                     bucket's entries are in buffer order.
-//   6. bkt_update     persistent CTAs claim buckets (queued big ones first,
-//                     then table-major order so each table's upstream slice
-//                     stays L2-resident).  Per bucket: stable counting sort by
-//                     row within the bucket (shared memory; <= 9-bit digits,
-//                     one pass for the usual bucket), row heads compacted by a
-//                     block scan, then a sub-warp of S lanes (8 row elements
-//                     per lane) per touched row: weight row + optimizer state
-//                     are prefetched, the row's upstream rows are gathered and
-//                     summed in order (two in flight), and one optimizer step
-//                     is applied and stored.  Rows with more than kLong
-//                     occurrences are split across every sub-warp of the CTA
-//                     (contiguous pieces, partials combined in piece order).
-//                     Buckets larger than kCap are sorted through global
-//                     scratch in kCap chunks by the same stable passes.
+//   6. bkt_sort       persistent CTAs claim buckets (queued big ones first,
+//                     then table-major order).  Per bucket: stable counting
+//                     sort by row within the bucket (shared memory; <= 9-bit
+//                     digits, one pass for the usual bucket; buckets larger
+//                     than kCap go through global scratch in kCap chunks by
+//                     the same stable passes), row heads compacted by a block
+//                     scan.  Rows with more occurrences than a stage holds are
+//                     split across every sub-warp of the CTA (contiguous
+//                     pieces, partials combined in piece order) and updated
+//                     here; the others are cut into row batches (consecutive
+//                     rows that fit one stage) appended to a batch stream.
+//   7. bkt_rows       persistent warp-specialised groups: a producer warp
+//                     stages each batch's weight rows, optimizer state and
+//                     upstream rows into shared memory with TMA bulk copies
+//                     (cp.async.bulk, byte-counted mbarrier), consumer warps
+//                     sum every row's upstream rows in order (sub-warp per
+//                     row) and apply one optimizer step, storing to HBM.
 //
 // Everything is deterministic: the order of every floating-point sum depends
 // only on the input.
@@ -62,6 +65,8 @@ constexpr int kMaxDim = kWarp * kEPL;
 constexpr int kScanTile = 4096;  // 256 threads x 16
 constexpr int kTarget = 1024;    // default occurrences per bucket
 static_assert(kUT == kBins, "one digit bin per update thread");
+static_assert(kBins * kUW * 2 >= kCap * 4, "batch list aliases the histograms");
+static_assert(kUW * kWarp * kEPL <= kCap, "long-row partials alias a sort buffer");
 
 struct Params {
   int32_t T;
@@ -79,7 +84,10 @@ struct Params {
   int32_t* big;      // queued big buckets
   int32_t* ctr;      // [0] claim counter, [1] big-bucket count
   uint32_t* ent;     // bucketed entries (row_low << bag_bits | bag)
-  uint32_t* ent2;    // scratch for big buckets
+  uint32_t* ent2;    // bucket entries sorted by row (read by the row kernel)
+  uint32_t* rrow;    // row records, dense per bucket: row in table
+  uint8_t* rlen;     //   ... its occurrences (0: a long row, updated by the sort kernel)
+  uint4* hdr;        // row batches: {first row record, first entry, rows | entries << 8, table}
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -301,9 +309,16 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
   const int64_t* off = q.offsets + (int64_t)t * q.B;
   const int64_t p0 = off[wb0], p1 = off[wb1];
   uint32_t* wh = hist + warp * nb;
-  for (int64_t p = p0 + lane; p < p1; p += kWarp) {
-    const int64_t id = (int64_t)indices[p];
-    if (id >= 0 && id < H) atomicAdd(&wh[(int)(id >> s)], 1u);
+  for (int64_t pb = p0; pb < p1; pb += 4 * kWarp) {  // four independent loads in flight per lane
+    int64_t id[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t p = pb + u * kWarp + lane;
+      id[u] = p < p1 ? (int64_t)indices[p] : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (id[u] >= 0 && id[u] < H) atomicAdd(&wh[(int)(id[u] >> s)], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
@@ -315,50 +330,62 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
     }
   }
   __syncthreads();
-  // place: 32 bags per window; each lane finds its entry's bag by a shuffle search
+  // place in buffer order: 32 bags per window, each lane finds its entry's
+  // bag by a shuffle search; ids of four rounds are loaded ahead
   for (int64_t bw = wb0; bw < wb1; bw += kWarp) {
     const int nbg = (int)min64(kWarp, wb1 - bw);
     const int64_t oend = off[bw + nbg];
     const int64_t o = lane < nbg ? off[bw + lane] : oend;
     const int64_t ostart = __shfl_sync(full, o, 0);
-    for (int64_t pb = ostart; pb < oend; pb += kWarp) {
-      const int64_t p = pb + lane;
-      const bool in = p < oend;
-      int k = 0;  // last bag of the window starting at or before p
+    for (int64_t pq = ostart; pq < oend; pq += 4 * kWarp) {
+      int64_t idq[4];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int64_t ok = __shfl_sync(full, o, k + step);
-        if (ok <= p) k += step;
+      for (int u = 0; u < 4; ++u) {
+        const int64_t p = pq + u * kWarp + lane;
+        idq[u] = p < oend ? (int64_t)indices[p] : -1;
       }
-      const int64_t id = in ? (int64_t)indices[p] : -1;
-      const bool valid = in && id >= 0 && id < H;
-      const uint32_t bk = valid ? (uint32_t)(id >> s) : 0xffffffffu;
-      const unsigned peers = __match_any_sync(full, bk);
-      if (valid) {
-        const uint32_t pos = wh[bk] + __popc(peers & lanemask_lt());
-        q.ent[pos] = (((uint32_t)id & rmask) << q.bag_bits) | (uint32_t)(bw + k);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t pb = pq + u * kWarp;
+        if (pb >= oend) break;  // warp-uniform
+        const int64_t p = pb + lane;
+        int k = 0;  // last bag of the window starting at or before p
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const int64_t ok = __shfl_sync(full, o, k + step);
+          if (ok <= p) k += step;
+        }
+        const int64_t id = idq[u];
+        const bool valid = p < oend && id >= 0 && id < H;
+        const uint32_t bk = valid ? (uint32_t)(id >> s) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(full, bk);
+        if (valid) {
+          const uint32_t pos = wh[bk] + __popc(peers & lanemask_lt());
+          q.ent[pos] = (((uint32_t)id & rmask) << q.bag_bits) | (uint32_t)(bw + k);
+        }
+        __syncwarp();
+        if (valid && (peers >> lane) == 1u) wh[bk] += __popc(peers);
+        __syncwarp();
       }
-      __syncwarp();
-      if (valid && (peers >> lane) == 1u) wh[bk] += __popc(peers);
-      __syncwarp();
     }
   }
 }
 
 // ---------------------------------------------------------------------------
-// 6. per-bucket sort + fused segment reduce + optimizer
+// 6. per-bucket row sort; hot rows updated here; short rows -> row batches
 
 struct alignas(16) USmem {
   uint32_t a[kCap];
   uint32_t b[kCap];
   int32_t rbeg[kCap + 1];
-  float part[kUW * kWarp * kEPL];
-  uint16_t hist[kBins * kUW];  // [bin][warp]
+  uint16_t hist[kBins * kUW];  // [bin][warp]; after the sort: the window's batches
   int32_t cursor[kBins];
   int32_t tot[kBins];
-  int32_t longs[kCap / kLong + 2];
+  int32_t longs[kCap / 2 + 2];
   int32_t wsum[kUW + 1];
   int32_t nlong;
+  int32_t nbat;
+  int32_t hbase;
   int32_t bucket;
   int32_t table;
   int32_t nrows;
@@ -559,45 +586,112 @@ __device__ __forceinline__ void finish_row(const RowCtx<W, G, OPT>& c, int64_t r
   if (col) st8<W>(c.wt + row * c.D + sl * kEPL, out);
 }
 
-// rows [0, nr) of the current window (starts in sm.rbeg): short rows one per
-// sub-warp, long rows split across the CTA
+// bytes one row batch occupies in a row-kernel stage
 template <typename W, typename G, int OPT>
-__device__ __forceinline__ void process_rows(const RowCtx<W, G, OPT>& c, const uint32_t* list, int nr, USmem& sm) {
+__host__ __device__ __forceinline__ int stage_row_bytes(int D) {
+  const int wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
+  const int mb = OPT == NEO_OPT_ROWWISE_ADAGRAD ? 16 : (OPT == NEO_OPT_ADAGRAD ? D * 4 : 0);
+  return wb + mb;
+}
+
+constexpr int kStageBytes = 24 * 1024;  // one row-kernel stage
+constexpr int kMaxRows = 32;            // rows per batch (one producer lane each)
+constexpr int kMaxEnt = 96;             // entries per batch (three producer loads per lane)
+
+// longest row staged by the row kernel; longer rows are updated by the sort kernel
+template <typename W, typename G, int OPT>
+__device__ __forceinline__ int long_threshold(int D) {
+  const int gb = D * (int)sizeof(G);
+  int lim = (kStageBytes - 32 - stage_row_bytes<W, G, OPT>(D)) / gb;
+  if (lim > kLong) lim = kLong;
+  return lim;
+}
+
+// window rows [0, nr) of list (starts in sm.rbeg): rows longer than the
+// threshold are split across the CTA and updated here; the others are cut
+// into batches (consecutive rows, <= kMaxRows rows, <= kMaxEnt entries,
+// <= kStageBytes staged bytes, never across a long row) appended to the
+// global batch stream for the row kernel
+template <typename W, typename G, int OPT>
+__device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Params& q, int t, int64_t bs,
+                                          int32_t rowidx0, const uint32_t* list, int nr, USmem& sm) {
   const unsigned full = 0xffffffffu;
   const int tid = threadIdx.x, warp = tid / kWarp, lane = tid % kWarp;
+  const int lth = long_threshold<W, G, OPT>(c.D);
+  const int rowb = stage_row_bytes<W, G, OPT>(c.D);
+  const int gb = c.D * (int)sizeof(G);
+  if (tid == 0) {
+    sm.nbat = 0;
+    sm.nlong = 0;
+  }
+  __syncthreads();
+  // row records (dense per bucket at bs + row index): row in table, length
+  for (int r = tid; r < nr; r += kUT) {
+    const int len = sm.rbeg[r + 1] - sm.rbeg[r];
+    const uint32_t row = (uint32_t)(c.row0 + (int64_t)(list[sm.rbeg[r]] >> c.bag_bits));
+    q.rrow[bs + rowidx0 + r] = row;
+    q.rlen[bs + rowidx0 + r] = (uint8_t)(len > lth ? 0 : len);
+  }
+  // greedy batching inside 32-row chunks, one warp per chunk; batches and
+  // long rows are appended in any order (each row is updated exactly once,
+  // so the order of batches does not change any result)
+  uint32_t* bat = reinterpret_cast<uint32_t*>(sm.hist);  // the sort's histograms are free now
+  const int nchunks = (nr + kWarp - 1) / kWarp;
+  for (int ck = warp; ck < nchunks; ck += kUW) {
+    const int cend = min(nr, ck * kWarp + kWarp);
+    int base = ck * kWarp;
+    while (base < cend) {
+      const int r = base + lane;
+      const bool v = r < cend;
+      const int len = v ? sm.rbeg[r + 1] - sm.rbeg[r] : 0;
+      const bool lg = v && len > lth;
+      const unsigned lgm = __ballot_sync(full, lg);
+      const int firstlong = lgm ? __ffs(lgm) - 1 : kWarp;
+      if (firstlong == 0) {
+        if (lane == 0) sm.longs[atomicAdd(&sm.nlong, 1)] = base;
+        ++base;
+        continue;
+      }
+      int cost = v && !lg ? rowb + len * gb : 0;  // + 32 bytes of region alignment below
+      int ent = v && !lg ? len : 0;
+#pragma unroll
+      for (int o = 1; o < kWarp; o <<= 1) {
+        const int x = __shfl_up_sync(full, cost, o), y = __shfl_up_sync(full, ent, o);
+        if (lane >= o) {
+          cost += x;
+          ent += y;
+        }
+      }
+      const bool fits = v && lane < firstlong && cost + 32 <= kStageBytes && ent <= kMaxEnt;
+      const int m = __popc(__ballot_sync(full, fits));  // >= 1: one short row always fits
+      if (lane == 0) bat[atomicAdd(&sm.nbat, 1)] = ((uint32_t)base << 8) | (uint32_t)m;
+      base += m;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) sm.hbase = sm.nbat ? atomicAdd(&q.ctr[2], sm.nbat) : 0;
+  __syncthreads();
+  for (int i = tid; i < sm.nbat; i += kUT) {
+    const uint32_t bw = bat[i];
+    const int r0 = (int)(bw >> 8), m = (int)(bw & 0xff);
+    const int e0 = sm.rbeg[r0], e1 = sm.rbeg[r0 + m];
+    uint4 h;
+    h.x = (uint32_t)(bs + rowidx0 + r0);   // first row record
+    h.y = (uint32_t)(bs + e0);             // first entry (sorted list in ent2)
+    h.z = (uint32_t)m | ((uint32_t)(e1 - e0) << 8);
+    h.w = (uint32_t)t;
+    q.hdr[sm.hbase + i] = h;
+  }
+  // long rows: every sub-warp of the CTA sums a contiguous piece, sub-warp 0
+  // of warp 0 combines the pieces in order and applies the step
   int S = 1;
   while (S * kEPL < c.D) S <<= 1;
   const int R = kWarp / S, sub = lane / S, sl = lane % S;
   const bool col = sl * kEPL < c.D;
-  if (tid == 0) sm.nlong = 0;
-  __syncthreads();
-  for (int g = warp; g * R < nr; g += kUW) {
-    const int r = g * R + sub;
-    bool valid = r < nr;
-    int64_t rb = 0, re = 0;
-    if (valid) {
-      rb = sm.rbeg[r];
-      re = sm.rbeg[r + 1];
-      if (re - rb > kLong) {
-        if (sl == 0) sm.longs[atomicAdd(&sm.nlong, 1)] = r;
-        valid = false;
-      }
-    }
-    const int64_t row = valid ? c.row0 + (int64_t)(list[rb] >> c.bag_bits) : 0;
-    float wv[kEPL], mv[kEPL], mrow;
-    prefetch_row<W, G, OPT>(c, row, valid, col, sl, wv, mv, mrow);
-    float acc[kEPL];
-#pragma unroll
-    for (int e = 0; e < kEPL; ++e) acc[e] = 0.f;
-    const int len = valid ? (int)(re - rb) : 0;
-    const int maxlen = (int)__reduce_max_sync(full, (unsigned)len);
-    gather_sum<W, G, OPT>(c, list, rb, rb + len, rb + maxlen, col && valid, sl, acc);
-    finish_row<W, G, OPT>(c, row, valid, col, S, sub, sl, wv, mv, mrow, acc);
-  }
-  __syncthreads();
   const int nl = sm.nlong;
   const int nsub = kUW * R;
   const int k = warp * R + sub;
+  float* part = reinterpret_cast<float*>(list == sm.a ? sm.b : sm.a);
   for (int l = 0; l < nl; ++l) {
     const int r = sm.longs[l];
     const int64_t rb = sm.rbeg[r], re = sm.rbeg[r + 1], len = re - rb;
@@ -610,10 +704,10 @@ __device__ __forceinline__ void process_rows(const RowCtx<W, G, OPT>& c, const u
     gather_sum<W, G, OPT>(c, list, a0, a1, a0 + span, col, sl, acc);
     if (col) {
 #pragma unroll
-      for (int e = 0; e < kEPL; ++e) sm.part[(k * S + sl) * kEPL + e] = acc[e];
+      for (int e = 0; e < kEPL; ++e) part[(k * S + sl) * kEPL + e] = acc[e];
     }
     __syncthreads();
-    if (warp == 0) {  // sub-warp 0 combines the partials in piece order, then one step
+    if (warp == 0) {
       const bool own = sub == 0;
       float wv[kEPL], mv[kEPL], mrow;
       prefetch_row<W, G, OPT>(c, row, own, col, sl, wv, mv, mrow);
@@ -622,7 +716,7 @@ __device__ __forceinline__ void process_rows(const RowCtx<W, G, OPT>& c, const u
       if (own && col) {
         for (int qq = 0; qq < nsub; ++qq)
 #pragma unroll
-          for (int e = 0; e < kEPL; ++e) acc[e] += sm.part[(qq * S + sl) * kEPL + e];
+          for (int e = 0; e < kEPL; ++e) acc[e] += part[(qq * S + sl) * kEPL + e];
       }
       finish_row<W, G, OPT>(c, row, own, col, S, sub, sl, wv, mv, mrow, acc);
     }
@@ -631,7 +725,7 @@ __device__ __forceinline__ void process_rows(const RowCtx<W, G, OPT>& c, const u
 }
 
 template <typename W, typename G, int OPT>
-__global__ void __launch_bounds__(kUT, 2) bkt_update_kernel(Params q, SegParams p) {
+__global__ void __launch_bounds__(kUT, 2) bkt_sort_kernel(Params q, SegParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   USmem& sm = *reinterpret_cast<USmem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -689,8 +783,17 @@ __global__ void __launch_bounds__(kUT, 2) bkt_update_kernel(Params q, SegParams 
       sort_pass(list, dst, n, q.bag_bits + k * wbits, nbits, sm);
       list = dst;
     }
+    // the row kernel reads the sorted list from ent2
+    if (list != q.ent2 + bs) {
+      for (int64_t i = tid; i < n; i += kUT) q.ent2[bs + i] = list[i];
+      if (!small) {
+        __syncthreads();
+        list = q.ent2 + bs;
+      }
+    }
     // row windows of <= kCap entries: heads compacted by a block scan
     int64_t pos = 0;
+    int32_t rowidx0 = 0;
     while (pos < n) {
       const int64_t w1 = min64(n, pos + kCap);
       constexpr int kPer = kCap / kUT;
@@ -712,7 +815,7 @@ __global__ void __launch_bounds__(kUT, 2) bkt_update_kernel(Params q, SegParams 
       int ex = block_scan_excl<kUT>(__popc(hm), sm.wsum, &nr);
 #pragma unroll
       for (int j = 0; j < kPer; ++j)
-        if ((hm >> j) & 1u) sm.rbeg[ex++] = (int32_t)(i0 + j);
+        if ((hm >> j) & 1u) sm.rbeg[ex++] = (int32_t)(i0 + j - pos);
       if (tid == 0) {
         // end of the window's last row (it may run past the window)
         int64_t end = w1;
@@ -726,13 +829,361 @@ __global__ void __launch_bounds__(kUT, 2) bkt_update_kernel(Params q, SegParams 
           }
           end = lo;
         }
-        sm.rbeg[nr] = (int32_t)end;
+        sm.rbeg[nr] = (int32_t)(end - pos);
         sm.nrows = nr;
       }
       __syncthreads();
-      process_rows<W, G, OPT>(c, list, sm.nrows, sm);
-      pos = sm.rbeg[sm.nrows];
+      const int nrw = sm.nrows;
+      emit_rows<W, G, OPT>(c, q, t, bs + pos, rowidx0 - (int32_t)pos, list + pos, nrw, sm);
+      rowidx0 += nrw;
+      pos += sm.rbeg[nrw];
       __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// 7. row kernel: warp-specialised groups (one producer + kRC consumers) over
+// the batch stream.  The producer stages each batch's weight rows, optimizer
+// state and upstream rows into a shared-memory stage with TMA bulk copies
+// (cp.async.bulk, completion counted in bytes on the stage's mbarrier), the
+// consumers sum each row's upstream rows in order and apply one step.
+
+constexpr int kRG = 4;    // groups per CTA
+constexpr int kRC = 3;    // consumer warps per group
+constexpr int kRS = 2;    // stages per group
+constexpr int kRT = kRG * (1 + kRC) * kWarp;
+
+struct StageMeta {
+  int32_t m;       // rows (-1: end of stream)
+  int32_t nent;
+  int32_t t;
+  int32_t pad;
+  uint32_t row[kMaxRows];
+  uint16_t eoff[kMaxRows];
+  uint8_t len[kMaxRows];
+  uint8_t mdir[kMaxRows];  // 1: moment read straight from global (chunk past the end)
+};
+
+struct RowSmem {
+  uint64_t full[kRG][kRS];
+  uint64_t empty[kRG][kRS];
+  StageMeta meta[kRG][kRS];
+  alignas(128) unsigned char data[kRG][kRS][kStageBytes];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity), "r"(1000000)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st16_hint(void* gmem, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;\n" ::"l"(gmem), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
+
+template <typename W, typename G, int OPT>
+__global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
+  const unsigned full = 0xffffffffu;
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int g = warp / (1 + kRC), role = warp % (1 + kRC);  // role 0 = producer
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRG; ++i)
+      for (int s = 0; s < kRS; ++s) {
+        mbar_init(&sm.full[i][s], 1);
+        mbar_init(&sm.empty[i][s], kRC);
+      }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  constexpr int kVW = 16 / (int)sizeof(W);  // W elements per 16-byte vector
+  if (role == 0) {
+    // ------------------------------------------------------------ producer
+    const int64_t nhdr = q.ctr[2];
+    const int64_t P = (int64_t)gridDim.x * kRG;
+    const uint32_t bmask = (uint32_t)((1u << q.bag_bits) - 1u);
+    const G* gbase = reinterpret_cast<const G*>(p.grad);
+    int s = 0;
+    uint32_t ephase = 1;  // stages start empty
+    // the weights stream through L2 once; the upstream rows of the table in
+    // flight are re-read by every occurrence and must stay resident
+    const uint64_t pol_stream = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
+    int64_t i = (int64_t)blockIdx.x * kRG + g;
+    // batch i's header and records are in registers one iteration ahead
+    uint4 h = i < nhdr ? q.hdr[i] : make_uint4(0, 0, 0, 0);
+    uint32_t row_n = 0, bag_n[kMaxEnt / kWarp];
+    int len_n = 0;
+    auto load_batch = [&](const uint4& hh, bool ok) {
+      const int mm = (int)(hh.z & 0xff), ne = (int)(hh.z >> 8);
+      row_n = ok && lane < mm ? q.rrow[hh.x + lane] : 0u;
+      len_n = ok && lane < mm ? (int)q.rlen[hh.x + lane] : 0;
+#pragma unroll
+      for (int k = 0; k < kMaxEnt / kWarp; ++k) {
+        const int j = lane + k * kWarp;
+        bag_n[k] = ok && j < ne ? (q.ent2[hh.y + j] & bmask) : 0u;
+      }
+    };
+    load_batch(h, i < nhdr);
+    uint4 hn = i + P < nhdr ? q.hdr[i + P] : make_uint4(0, 0, 0, 0);
+    for (; i < nhdr; i += P) {
+      const uint32_t row = row_n;
+      const int len = len_n;
+      uint32_t bag[kMaxEnt / kWarp];
+#pragma unroll
+      for (int k = 0; k < kMaxEnt / kWarp; ++k) bag[k] = bag_n[k];
+      load_batch(hn, i + P < nhdr);  // next batch's records in flight while this one is issued
+      const uint4 hcur = h;
+      h = hn;
+      hn = i + 2 * P < nhdr ? q.hdr[i + 2 * P] : make_uint4(0, 0, 0, 0);
+      const int m = (int)(hcur.z & 0xff), nent = (int)(hcur.z >> 8), t = (int)hcur.w;
+      const int32_t doff = p.dim_offsets[t];
+      const int D = p.dim_offsets[t + 1] - doff;
+      const int64_t H = p.row_offsets[t + 1] - p.row_offsets[t];
+      const int wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
+      const int mb = OPT == NEO_OPT_ROWWISE_ADAGRAD ? 16 : (OPT == NEO_OPT_ADAGRAD ? D * 4 : 0);
+      const int gb = D * (int)sizeof(G);
+      int eoff = len;
+#pragma unroll
+      for (int o = 1; o < kWarp; o <<= 1) {
+        const int x = __shfl_up_sync(full, eoff, o);
+        if (lane >= o) eoff += x;
+      }
+      eoff -= len;
+      const bool mdir = OPT == NEO_OPT_ROWWISE_ADAGRAD && (int64_t)(row | 3u) >= H;
+      const uint32_t mdv = __ballot_sync(full, lane < m && mdir);
+      mbar_wait(&sm.empty[g][s], ephase);
+      StageMeta& mt = sm.meta[g][s];
+      if (lane < m) {
+        mt.row[lane] = row;
+        mt.eoff[lane] = (uint16_t)eoff;
+        mt.len[lane] = (uint8_t)len;
+        mt.mdir[lane] = mdir ? 1 : 0;
+      }
+      if (lane == 0) {
+        mt.m = m;
+        mt.nent = nent;
+        mt.t = t;
+      }
+      __syncwarp();
+      const uint32_t bytes = (uint32_t)(m * wb + (m - __popc(mdv)) * mb + nent * gb);
+      if (lane == 0) mbar_arrive_tx(&sm.full[g][s], bytes);
+      __syncwarp();
+      unsigned char* st = sm.data[g][s];
+      uint64_t* fb = &sm.full[g][s];
+      if (lane < m) {
+        if (OPT != NEO_OPT_NONE)
+          bulk_g2s(st + lane * wb, reinterpret_cast<const W*>(p.weights[t]) + (int64_t)row * D, wb, fb, pol_stream);
+        const float* mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD)
+                               ? reinterpret_cast<const float*>(p.moments[t])
+                               : nullptr;
+        if (OPT == NEO_OPT_ROWWISE_ADAGRAD && !mdir)
+          bulk_g2s(st + m * wb + lane * 16, mom + (row & ~3u), 16, fb, pol_stream);
+        if (OPT == NEO_OPT_ADAGRAD) bulk_g2s(st + m * wb + lane * mb, mom + (int64_t)row * D, mb, fb, pol_stream);
+      }
+      unsigned char* gst = st + ((m * (wb + mb) + 31) & ~31);
+#pragma unroll
+      for (int k = 0; k < kMaxEnt / kWarp; ++k) {
+        const int j = lane + k * kWarp;
+        if (j < nent) bulk_g2s(gst + j * gb, gbase + (int64_t)bag[k] * p.grad_stride + doff, gb, fb, pol_keep);
+      }
+      if (++s == kRS) {
+        s = 0;
+        ephase ^= 1;
+      }
+    }
+    // end of stream
+    mbar_wait(&sm.empty[g][s], ephase);
+    if (lane == 0) {
+      sm.meta[g][s].m = -1;
+      mbar_arrive(&sm.full[g][s]);
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumer
+  // a sub-warp of S lanes per row; lane sl owns the row's 16-byte W vectors
+  // v*S + sl (v < kLV: kEL elements per lane, interleaved so every shared-
+  // memory access of a sub-warp is contiguous), R = 32/S rows per warp
+  constexpr int kEL = 16;
+  constexpr int kLV = kEL / kVW;
+  const int c = role - 1;
+  const uint64_t pol_stream = policy_evict_first();
+  const float lr = (float)p.lr, eps = (float)p.eps;
+  int s = 0;
+  uint32_t fphase = 0;
+  for (;;) {
+    mbar_wait(&sm.full[g][s], fphase);
+    const StageMeta& mt = sm.meta[g][s];
+    const int m = mt.m;
+    if (m < 0) break;
+    const int t = mt.t;
+    const int D = p.dim_offsets[t + 1] - p.dim_offsets[t];
+    const int wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
+    const int mb = OPT == NEO_OPT_ROWWISE_ADAGRAD ? 16 : (OPT == NEO_OPT_ADAGRAD ? D * 4 : 0);
+    const int gb = D * (int)sizeof(G);
+    const int nv = D / kVW;  // 16-byte W vectors per row
+    int S = 1;
+    while (S * kLV < nv) S <<= 1;
+    const int R = kWarp / S, sub = lane / S, sl = lane % S;
+    const unsigned submask = S == kWarp ? full : (((1u << S) - 1u) << (sub * S));
+    const unsigned char* st = sm.data[g][s];
+    const unsigned char* gst = st + ((m * (wb + mb) + 31) & ~31);
+    W* wt = reinterpret_cast<W*>(OPT == NEO_OPT_NONE ? p.dense_grads[t] : p.weights[t]);
+    float* mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD) ? reinterpret_cast<float*>(p.moments[t])
+                                                                           : nullptr;
+    const float invD = 1.0f / (float)D;
+    const int rounds = (m + kRC * R - 1) / (kRC * R);
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int rr = (rd * kRC + c) * R + sub;
+      const bool valid = rr < m;
+      const int len = valid ? mt.len[rr] : 0;
+      const int eo = valid ? mt.eoff[rr] : 0;
+      const uint32_t row = valid ? mt.row[rr] : 0u;
+      const int maxlen = (int)__reduce_max_sync(full, (unsigned)len);
+      float acc[kLV][kVW];
+#pragma unroll
+      for (int v = 0; v < kLV; ++v)
+#pragma unroll
+        for (int e = 0; e < kVW; ++e) acc[v][e] = 0.f;
+      const G* gr = reinterpret_cast<const G*>(gst + eo * gb);
+      for (int j = 0; j < maxlen; ++j) {  // the row's upstream rows, in order
+        if (j < len) {
+#pragma unroll
+          for (int v = 0; v < kLV; ++v) {
+            const int vi = v * S + sl;
+            if (vi < nv) {
+              Vec<G, kVW> x;
+              if constexpr (sizeof(G) * kVW == 32) {
+                reinterpret_cast<uint4*>(&x)[0] = reinterpret_cast<const uint4*>(gr + vi * kVW)[0];
+                reinterpret_cast<uint4*>(&x)[1] = reinterpret_cast<const uint4*>(gr + vi * kVW)[1];
+              } else {
+                x = *reinterpret_cast<const Vec<G, kVW>*>(gr + vi * kVW);
+              }
+#pragma unroll
+              for (int e = 0; e < kVW; ++e) acc[v][e] += Elem<G>::to_f(x.v[e]);
+            }
+          }
+        }
+        gr += D;
+      }
+      if (OPT == NEO_OPT_NONE) {
+        if (valid) {
+#pragma unroll
+          for (int v = 0; v < kLV; ++v) {
+            const int vi = v * S + sl;
+            if (vi < nv) {
+              float* dst = reinterpret_cast<float*>(wt) + (int64_t)row * D + vi * kVW;
+#pragma unroll
+              for (int e = 0; e < kVW; e += 4)
+                *reinterpret_cast<float4*>(dst + e) =
+                    make_float4(acc[v][e], acc[v][e + 1], acc[v][e + 2], acc[v][e + 3]);
+            }
+          }
+        }
+        continue;
+      }
+      float ss = 0.f;
+      if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
+#pragma unroll
+        for (int v = 0; v < kLV; ++v)
+#pragma unroll
+          for (int e = 0; e < kVW; ++e) ss += acc[v][e] * acc[v][e];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+          if (o < S) ss += __shfl_xor_sync(full, ss, o);
+      }
+      bool live = valid;
+      if (OPT == NEO_OPT_ADAGRAD || OPT == NEO_OPT_ROWWISE_ADAGRAD) {
+        // an identically zero gradient leaves the row untouched (embedding.py:223-228)
+        bool nz = false;
+#pragma unroll
+        for (int v = 0; v < kLV; ++v)
+#pragma unroll
+          for (int e = 0; e < kVW; ++e) nz |= acc[v][e] != 0.f;
+        const unsigned vote = __ballot_sync(full, nz);
+        live = live && (vote & submask) != 0u;
+      }
+      if (!live) continue;
+      float scale = lr;
+      if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
+        const float mr = mt.mdir[rr] ? mom[row]
+                                     : reinterpret_cast<const float*>(st + m * wb + rr * 16)[row & 3u];
+        const float mn = mr + ss * invD;
+        if (sl == 0) mom[row] = mn;
+        scale = __fdividef(lr, __fsqrt_rn(mn) + eps);
+      }
+#pragma unroll
+      for (int v = 0; v < kLV; ++v) {
+        const int vi = v * S + sl;
+        if (vi < nv) {
+          const Vec<W, kVW> w = *reinterpret_cast<const Vec<W, kVW>*>(st + rr * wb + vi * 16);
+          Vec<W, kVW> o;
+          if (OPT == NEO_OPT_ADAGRAD) {
+            const float* mv = reinterpret_cast<const float*>(st + m * wb + rr * mb) + vi * kVW;
+            float mo[kVW];
+#pragma unroll
+            for (int e = 0; e < kVW; ++e) {
+              mo[e] = mv[e] + acc[v][e] * acc[v][e];
+              o.v[e] = Elem<W>::from_f(Elem<W>::to_f(w.v[e]) -
+                                       __fdividef(lr * acc[v][e], __fsqrt_rn(mo[e]) + eps));
+            }
+            float* md = mom + (int64_t)row * D + vi * kVW;
+#pragma unroll
+            for (int e = 0; e < kVW; e += 4)
+              *reinterpret_cast<float4*>(md + e) = make_float4(mo[e], mo[e + 1], mo[e + 2], mo[e + 3]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < kVW; ++e) o.v[e] = Elem<W>::from_f(Elem<W>::to_f(w.v[e]) - acc[v][e] * scale);
+          }
+          st16_hint(wt + (int64_t)row * D + vi * kVW, *reinterpret_cast<const uint4*>(&o), pol_stream);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[g][s]);
+    if (++s == kRS) {
+      s = 0;
+      fphase ^= 1;
     }
   }
 }
@@ -762,28 +1213,42 @@ static int dbg(cudaStream_t s, const char* what) {
 }
 
 template <typename W, typename G, int OPT>
-static int launch_update(const Params& q, const SegParams& p, int sms, cudaStream_t s) {
-  auto kern = bkt_update_kernel<W, G, OPT>;
-  const int smem = (int)sizeof(USmem);
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve bucket shared memory");
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kUT, smem);
-  if (per_sm < 1) per_sm = 1;
-  kern<<<(unsigned)(sms * per_sm), kUT, smem, s>>>(q, p);
-  return dbg(s, "neo_tbe_backward(bucket update)");
+static int launch_update(const Params& q, const SegParams& p, int sms, cudaStream_t s, bool prepare, bool apply) {
+  if (prepare) {
+    auto kern = bkt_sort_kernel<W, G, OPT>;
+    const int smem = (int)sizeof(USmem);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve bucket shared memory");
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kUT, smem);
+    if (per_sm < 1) per_sm = 1;
+    kern<<<(unsigned)(sms * per_sm), kUT, smem, s>>>(q, p);
+    const int rc = dbg(s, "neo_tbe_backward(bucket sort)");
+    if (rc) return rc;
+  }
+  if (apply) {
+    auto kern = bkt_rows_kernel<W, G, OPT>;
+    const int smem = (int)sizeof(RowSmem);
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve row-kernel shared memory");
+    kern<<<(unsigned)sms, kRT, smem, s>>>(q, p);
+    return dbg(s, "neo_tbe_backward(bucket rows)");
+  }
+  return NEO_OK;
 }
 
 template <typename W, typename G>
-static int launch_update_opt(const Params& q, const SegParams& p, int sms, cudaStream_t s) {
+static int launch_update_opt(const Params& q, const SegParams& p, int sms, cudaStream_t s, bool prepare,
+                             bool apply) {
   if (p.mode == NEO_BWD_DENSE) {
-    if constexpr (std::is_same<W, float>::value) return launch_update<W, G, NEO_OPT_NONE>(q, p, sms, s);
+    if constexpr (std::is_same<W, float>::value)
+      return launch_update<W, G, NEO_OPT_NONE>(q, p, sms, s, prepare, apply);
     return fail(NEO_E_ARG, "neo_tbe_backward: DENSE needs f32");
   }
   switch (p.optim) {
-    case NEO_OPT_SGD: return launch_update<W, G, NEO_OPT_SGD>(q, p, sms, s);
-    case NEO_OPT_ROWWISE_ADAGRAD: return launch_update<W, G, NEO_OPT_ROWWISE_ADAGRAD>(q, p, sms, s);
-    default: return launch_update<W, G, NEO_OPT_ADAGRAD>(q, p, sms, s);
+    case NEO_OPT_SGD: return launch_update<W, G, NEO_OPT_SGD>(q, p, sms, s, prepare, apply);
+    case NEO_OPT_ROWWISE_ADAGRAD: return launch_update<W, G, NEO_OPT_ROWWISE_ADAGRAD>(q, p, sms, s, prepare, apply);
+    default: return launch_update<W, G, NEO_OPT_ADAGRAD>(q, p, sms, s, prepare, apply);
   }
 }
 
@@ -800,6 +1265,7 @@ size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows) {
   const int64_t cpt = (B + kCHB - 1) / kCHB;
   const int64_t nb = bucket_bound(T, total_rows);
   const int64_t M = nb * cpt;
+  const int64_t n1 = N > 0 ? N : 1;
   size_t b = 0;
   b += align256(sizeof(int32_t) * T);                    // sbits
   b += align256(sizeof(int64_t) * (T + 1));              // bbase
@@ -808,7 +1274,10 @@ size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows) {
   b += align256(sizeof(int32_t) * (nb + 1));             // bucket starts
   b += align256(sizeof(int32_t) * (nb + 1));             // big-bucket queue
   b += align256(sizeof(int32_t) * 4);                    // counters
-  b += 2 * align256(sizeof(uint32_t) * (N > 0 ? N : 1));  // entries + scratch
+  b += 2 * align256(sizeof(uint32_t) * n1);              // entries + sorted entries
+  b += align256(sizeof(uint32_t) * n1);                  // row records: row
+  b += align256(sizeof(uint8_t) * n1);                   // row records: length
+  b += align256(sizeof(uint4) * n1);                     // batch headers (<= one per entry)
   return b;
 }
 
@@ -818,7 +1287,6 @@ bool bkt_eligible(const SegParams& p, int32_t weight_dtype, int32_t grad_dtype, 
   const char* v = std::getenv("NEO_BWD_VARIANT");
   if (v && (std::strcmp(v, "pipe") == 0 || std::strcmp(v, "stream") == 0)) return false;
   if (!(p.flags & NEO_BWD_FLAG_DIM8) || out_count) return false;
-  if (p.flags & (NEO_BWD_FLAG_PREPARE | NEO_BWD_FLAG_APPLY)) return false;
   if (p.pooling != NEO_POOL_SUM || p.max_dim > kMaxDim) return false;
   if (grad_dtype != NEO_F32 && grad_dtype != NEO_BF16 && grad_dtype != NEO_F16) return false;
   if (p.mode == NEO_BWD_UPDATE) {
@@ -831,7 +1299,7 @@ bool bkt_eligible(const SegParams& p, int32_t weight_dtype, int32_t grad_dtype, 
   // the bucket bits of the largest possible table (kMaxB buckets) + bag bits must fit 32
   int s = kSMin;
   while (((p.total_rows + (int64_t(1) << s) - 1) >> s) > kMaxB) ++s;
-  return s + bag_bits_for(p.B) <= 32;
+  return s + bag_bits_for(p.B) <= 32 && p.N < (int64_t(1) << 31);
 }
 
 int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, const void* indices,
@@ -850,6 +1318,7 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
   q.offsets = p.offsets;
   const int64_t nb = bucket_bound(p.T, p.total_rows);
   const int64_t M = nb * q.cpt;
+  const int64_t n1 = N > 0 ? N : 1;
   unsigned char* w = static_cast<unsigned char*>(workspace);
   q.sbits = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * p.T);
@@ -866,29 +1335,39 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
   q.ctr = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * 4);
   q.ent = reinterpret_cast<uint32_t*>(w);
-  w += align256(sizeof(uint32_t) * (N > 0 ? N : 1));
+  w += align256(sizeof(uint32_t) * n1);
   q.ent2 = reinterpret_cast<uint32_t*>(w);
+  w += align256(sizeof(uint32_t) * n1);
+  q.rrow = reinterpret_cast<uint32_t*>(w);
+  w += align256(sizeof(uint32_t) * n1);
+  q.rlen = reinterpret_cast<uint8_t*>(w);
+  w += align256(sizeof(uint8_t) * n1);
+  q.hdr = reinterpret_cast<uint4*>(w);
 
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  bkt_setup_kernel<<<1, 1024, 0, s>>>(q);
-  int rc = dbg(s, "neo_tbe_backward(bucket setup)");
-  if (rc) return rc;
-  const unsigned chunks = (unsigned)(p.T * (int64_t)q.cpt);
-  if (index_dtype == NEO_I32)
-    bkt_count_kernel<int32_t><<<chunks, kScW * kWarp, 0, s>>>(q, (const int32_t*)indices, err);
-  else
-    bkt_count_kernel<int64_t><<<chunks, kScW * kWarp, 0, s>>>(q, (const int64_t*)indices, err);
-  if ((rc = dbg(s, "neo_tbe_backward(bucket count)"))) return rc;
-  const unsigned tiles = (unsigned)((M + kScanTile - 1) / kScanTile);
-  bkt_scan_reduce_kernel<<<tiles > 0 ? tiles : 1, 256, 0, s>>>(q);
-  bkt_scan_tiles_kernel<<<1, 1024, 0, s>>>(q);
-  bkt_scan_down_kernel<<<tiles > 0 ? tiles : 1, 256, 0, s>>>(q);
-  if ((rc = dbg(s, "neo_tbe_backward(bucket scan)"))) return rc;
-  bkt_classify_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(q);
-  if ((rc = dbg(s, "neo_tbe_backward(bucket classify)"))) return rc;
-  {
+  // PREPARE = the sort phase (counting sort + batches; hot rows are updated
+  // here), APPLY = the row kernel; the state between them is the workspace
+  const bool prepare = !(p.flags & NEO_BWD_FLAG_APPLY);
+  const bool apply = !(p.flags & NEO_BWD_FLAG_PREPARE);
+  int rc = NEO_OK;
+  if (prepare) {
+    bkt_setup_kernel<<<1, 1024, 0, s>>>(q);
+    if ((rc = dbg(s, "neo_tbe_backward(bucket setup)"))) return rc;
+    const unsigned chunks = (unsigned)(p.T * (int64_t)q.cpt);
+    if (index_dtype == NEO_I32)
+      bkt_count_kernel<int32_t><<<chunks, kScW * kWarp, 0, s>>>(q, (const int32_t*)indices, err);
+    else
+      bkt_count_kernel<int64_t><<<chunks, kScW * kWarp, 0, s>>>(q, (const int64_t*)indices, err);
+    if ((rc = dbg(s, "neo_tbe_backward(bucket count)"))) return rc;
+    const unsigned tiles = (unsigned)((M + kScanTile - 1) / kScanTile);
+    bkt_scan_reduce_kernel<<<tiles > 0 ? tiles : 1, 256, 0, s>>>(q);
+    bkt_scan_tiles_kernel<<<1, 1024, 0, s>>>(q);
+    bkt_scan_down_kernel<<<tiles > 0 ? tiles : 1, 256, 0, s>>>(q);
+    if ((rc = dbg(s, "neo_tbe_backward(bucket scan)"))) return rc;
+    bkt_classify_kernel<<<(unsigned)((nb + 255) / 256), 256, 0, s>>>(q);
+    if ((rc = dbg(s, "neo_tbe_backward(bucket classify)"))) return rc;
     const int smem = (int)((kScW + 1) * kMaxB * sizeof(uint32_t));
     auto k32 = bkt_scatter_kernel<int32_t>;
     auto k64 = bkt_scatter_kernel<int64_t>;
@@ -898,23 +1377,25 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
     if (index_dtype == NEO_I32) k32<<<chunks, kScW * kWarp, smem, s>>>(q, (const int32_t*)indices);
     else k64<<<chunks, kScW * kWarp, smem, s>>>(q, (const int64_t*)indices);
     if ((rc = dbg(s, "neo_tbe_backward(bucket scatter)"))) return rc;
+    launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
+    if ((rc = check_launch("neo_tbe_backward(finalize)"))) return rc;
   }
   const bool h = weight_dtype == NEO_F16;
   switch (grad_dtype) {
     case NEO_F32:
-      rc = h ? launch_update_opt<__half, float>(q, p, sms, s) : launch_update_opt<float, float>(q, p, sms, s);
+      rc = h ? launch_update_opt<__half, float>(q, p, sms, s, prepare, apply)
+             : launch_update_opt<float, float>(q, p, sms, s, prepare, apply);
       break;
     case NEO_BF16:
-      rc = h ? launch_update_opt<__half, __nv_bfloat16>(q, p, sms, s)
-             : launch_update_opt<float, __nv_bfloat16>(q, p, sms, s);
+      rc = h ? launch_update_opt<__half, __nv_bfloat16>(q, p, sms, s, prepare, apply)
+             : launch_update_opt<float, __nv_bfloat16>(q, p, sms, s, prepare, apply);
       break;
     default:
-      rc = h ? launch_update_opt<__half, __half>(q, p, sms, s) : launch_update_opt<float, __half>(q, p, sms, s);
+      rc = h ? launch_update_opt<__half, __half>(q, p, sms, s, prepare, apply)
+             : launch_update_opt<float, __half>(q, p, sms, s, prepare, apply);
       break;
   }
-  if (rc) return rc;
-  launch_error_finalize(err, indices, index_dtype, p.offsets, p.B, p.T, s);
-  return check_launch("neo_tbe_backward(finalize)");
+  return rc;
 }
 
 }  // namespace neo

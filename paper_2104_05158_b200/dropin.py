@@ -69,9 +69,14 @@ def install(neosim=None):
     table = {k: getattr(_emb, {"sgd": "apply_sgd", "rowwise_adagrad": "apply_rowwise_adagrad",
                                "adagrad": "apply_adagrad"}[k.value]) for k in emb.OptimizerKind}
     _set(emb, "_OPTIMIZERS", table)
-    # results are built with the reference's own types
+    # results are built with the reference's own types (identity checks such
+    # as `layout.tag is LayoutTag.TWB` in the unpatched from_twb must hold)
     _set(_emb, "RowGradients", emb.RowGradients)
     _set(_emb, "EmbeddingTable", emb.EmbeddingTable)
+    for name in ("CombinedBatch", "GlobalBatchLayout", "LayoutTag", "LaidOutBatch", "ShardInput", "WorkerSlice",
+                 "ShardedState"):
+        if hasattr(com, name):
+            _set(_comms, name, getattr(com, name))
     for name in _EMBEDDING:
         _set(emb, name, getattr(_emb, name))
         if hasattr(neosim, name):

@@ -224,14 +224,19 @@ class TableGroup:
             n_b = n_idx if table_counts is None else int(sum(table_counts))
             wsb = capi.lib().neo_tbe_bucket_workspace_bytes(self.T, batch, max(n_b, 1), self.total_rows)
             ws = WORKSPACE.get("tbe_bucket", wsb, self.device)
-            if timers is not None:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-            self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling, err, 0,
-                                self.T, None, None, None, None, dense_ptrs, n_b, ws=ws)
-            if timers is not None:
-                e1.record()
-                timers.setdefault("apply", []).append((e0, e1, 0, self.T))
+            if timers is None:
+                self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling, err,
+                                    0, self.T, None, None, None, None, dense_ptrs, n_b, ws=ws)
+                return None
+            # timed: the sort phase and the fused update kernel as two calls
+            self._backward_call(indices, offsets, batch, grad, stride, mode_code | capi.NEO_BWD_FLAG_PREPARE, optim,
+                                lr, eps, pooling, err, 0, self.T, None, None, None, None, dense_ptrs, n_b, ws=ws)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            self._backward_call(indices, offsets, batch, grad, stride, mode_code | capi.NEO_BWD_FLAG_APPLY, optim,
+                                lr, eps, pooling, err, 0, self.T, None, None, None, None, dense_ptrs, n_b, ws=ws)
+            e1.record()
+            timers.setdefault("apply", []).append((e0, e1, 0, self.T))
             return None
         prep = getattr(self, "_prepared", None)
         if (mode == "update" and prep is not None and prep["key"] == (indices.data_ptr(), offsets.data_ptr(), batch)
