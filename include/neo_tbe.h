@@ -166,7 +166,7 @@ int neo_tbe_forward_scatter(int32_t num_tables, int64_t batch,
 size_t neo_tbe_backward_workspace_bytes(int64_t num_indices, int64_t total_rows, int32_t max_dim);
 /* workspace of the bucketed path (NEO_BWD_FLAG_DIM8) for T tables of B bags */
 size_t neo_tbe_bucket_workspace_bytes(int32_t num_tables, int64_t batch, int64_t num_indices,
-                                      int64_t total_rows);
+                                      int64_t total_rows, int32_t max_dim);
 
 int neo_tbe_backward(int32_t num_tables, int64_t batch,
                      const int64_t* row_offsets, int64_t total_rows,

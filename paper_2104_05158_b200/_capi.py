@@ -69,7 +69,7 @@ SIGNATURES = {
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I64, I32, I64, P, P],
     ),
     "neo_tbe_backward_workspace_bytes": (SZ, [I64, I64, I32]),
-    "neo_tbe_bucket_workspace_bytes": (SZ, [I32, I64, I64, I64]),
+    "neo_tbe_bucket_workspace_bytes": (SZ, [I32, I64, I64, I64, I32]),
     "neo_tbe_backward": (
         C.c_int,
         [I32, I64, P, I64, P, I32, P, I32, P, P, I32, P, I64, I32, P, I32, I64,

@@ -47,7 +47,7 @@ struct SegParams {
 
 // bucketed path (tbe_bucket.cu)
 bool bkt_eligible(const SegParams& p, int32_t weight_dtype, int32_t grad_dtype, bool out_count);
-size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows);
+size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows, int32_t max_dim);
 int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, const void* indices,
                         int32_t index_dtype, void* workspace, size_t ws_bytes, neo_error* err, cudaStream_t s);
 

@@ -42,6 +42,8 @@
 //
 // Everything is deterministic: the order of every floating-point sum depends
 // only on the input.
+#include <cuda.h>
+
 #include <cstdio>
 #include <string>
 
@@ -82,12 +84,15 @@ struct Params {
   int32_t* tiles;    // scan tile sums
   int32_t* bstart;   // [nb+1]
   int32_t* big;      // queued big buckets
-  int32_t* ctr;      // [0] claim counter, [1] big-bucket count
+  int32_t* ctr;      // [0] claim counter, [1] big-bucket count, [2] batches, [3] record units,
+                     // [4] capacity overflow
   uint32_t* ent;     // bucketed entries (row_low << bag_bits | bag)
   uint32_t* ent2;    // bucket entries sorted by row (read by the row kernel)
-  uint32_t* rrow;    // row records, dense per bucket: row in table
-  uint8_t* rlen;     //   ... its occurrences (0: a long row, updated by the sort kernel)
-  uint4* hdr;        // row batches: {first row record, first entry, rows | entries << 8, table}
+  uint32_t* rec;     // row-batch records (16-byte units): {rows | entries << 8, table, -, -}, rows,
+                     // row lengths (bytes), bags (entries padded to 4)
+  uint2* hdr;        // per batch: {record offset, record size} in 16-byte units
+  int64_t rec_cap;   // capacity of rec in 16-byte units
+  int64_t hdr_cap;   // capacity of hdr
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -141,7 +146,7 @@ __global__ void __launch_bounds__(1024) bkt_setup_kernel(Params q) {
   __shared__ int wsum[33];
   __shared__ long long s_carry;
   if (threadIdx.x == 0) s_carry = 0;
-  if (threadIdx.x < 4) q.ctr[threadIdx.x] = 0;
+  if (threadIdx.x < 8) q.ctr[threadIdx.x] = 0;
   __syncthreads();
   for (int t0 = 0; t0 < q.T; t0 += 1024) {
     const int t = t0 + threadIdx.x;
@@ -386,6 +391,7 @@ struct alignas(16) USmem {
   int32_t nlong;
   int32_t nbat;
   int32_t hbase;
+  int32_t rbase16;  // record base of the window
   int32_t bucket;
   int32_t table;
   int32_t nrows;
@@ -586,23 +592,37 @@ __device__ __forceinline__ void finish_row(const RowCtx<W, G, OPT>& c, int64_t r
   if (col) st8<W>(c.wt + row * c.D + sl * kEPL, out);
 }
 
-// bytes one row batch occupies in a row-kernel stage
+// bytes one row batch occupies in a row-kernel stage: per row the weight row
+// (+ its element-wise state); per stage 128 bytes of alignment and, for the
+// row-wise state, a moment span of up to kMomSpan bytes
+constexpr int kMomSpan = 1024;
 template <typename W, typename G, int OPT>
 __host__ __device__ __forceinline__ int stage_row_bytes(int D) {
   const int wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
-  const int mb = OPT == NEO_OPT_ROWWISE_ADAGRAD ? 16 : (OPT == NEO_OPT_ADAGRAD ? D * 4 : 0);
-  return wb + mb;
+  return wb + (OPT == NEO_OPT_ADAGRAD ? D * 4 : 0);
+}
+template <int OPT>
+__host__ __device__ __forceinline__ int stage_fixed_bytes() {
+  return 128 + (OPT == NEO_OPT_ROWWISE_ADAGRAD ? kMomSpan : 0);
 }
 
-constexpr int kStageBytes = 24 * 1024;  // one row-kernel stage
+#ifndef NEO_BKT_STAGE_KB
+#define NEO_BKT_STAGE_KB 24
+#endif
+constexpr int kStageBytes = NEO_BKT_STAGE_KB * 1024;  // one row-kernel stage
 constexpr int kMaxRows = 32;            // rows per batch (one producer lane each)
-constexpr int kMaxEnt = 96;             // entries per batch (three producer loads per lane)
+constexpr int kMaxEnt = 96;             // entries per batch (gather4 groups: <= 24)
+constexpr int kRecMax16 = 1 + kMaxRows / 4 + kMaxRows / 16 + kMaxEnt / 4;  // record size bound (16-byte units)
+
+__host__ __device__ __forceinline__ int rec_units(int m, int nent) {
+  return 1 + (m + 3) / 4 + (m + 15) / 16 + (nent + 3) / 4;
+}
 
 // longest row staged by the row kernel; longer rows are updated by the sort kernel
 template <typename W, typename G, int OPT>
 __device__ __forceinline__ int long_threshold(int D) {
   const int gb = D * (int)sizeof(G);
-  int lim = (kStageBytes - 32 - stage_row_bytes<W, G, OPT>(D)) / gb;
+  int lim = (kStageBytes - stage_fixed_bytes<OPT>() - stage_row_bytes<W, G, OPT>(D)) / gb - 3;  // padded to 4
   if (lim > kLong) lim = kLong;
   return lim;
 }
@@ -625,13 +645,6 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
     sm.nlong = 0;
   }
   __syncthreads();
-  // row records (dense per bucket at bs + row index): row in table, length
-  for (int r = tid; r < nr; r += kUT) {
-    const int len = sm.rbeg[r + 1] - sm.rbeg[r];
-    const uint32_t row = (uint32_t)(c.row0 + (int64_t)(list[sm.rbeg[r]] >> c.bag_bits));
-    q.rrow[bs + rowidx0 + r] = row;
-    q.rlen[bs + rowidx0 + r] = (uint8_t)(len > lth ? 0 : len);
-  }
   // greedy batching inside 32-row chunks, one warp per chunk; batches and
   // long rows are appended in any order (each row is updated exactly once,
   // so the order of batches does not change any result)
@@ -652,7 +665,7 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
         ++base;
         continue;
       }
-      int cost = v && !lg ? rowb + len * gb : 0;  // + 32 bytes of region alignment below
+      int cost = v && !lg ? rowb + len * gb : 0;  // + 128 bytes of region alignment below
       int ent = v && !lg ? len : 0;
 #pragma unroll
       for (int o = 1; o < kWarp; o <<= 1) {
@@ -662,26 +675,67 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
           ent += y;
         }
       }
-      const bool fits = v && lane < firstlong && cost + 32 <= kStageBytes && ent <= kMaxEnt;
+      const bool fits =
+          v && lane < firstlong && cost + stage_fixed_bytes<OPT>() + 3 * gb <= kStageBytes && ent <= kMaxEnt;
       const int m = __popc(__ballot_sync(full, fits));  // >= 1: one short row always fits
       if (lane == 0) bat[atomicAdd(&sm.nbat, 1)] = ((uint32_t)base << 8) | (uint32_t)m;
       base += m;
     }
   }
   __syncthreads();
-  if (tid == 0) sm.hbase = sm.nbat ? atomicAdd(&q.ctr[2], sm.nbat) : 0;
+  // records: offsets by a block scan over the window's batches, one
+  // reservation per window, then one warp writes each record
+  const int nbat = sm.nbat;
+  uint32_t* roff = reinterpret_cast<uint32_t*>(list == sm.a ? sm.b : sm.a);  // free sort buffer
+  {
+    int carry = 0;
+    for (int i0 = 0; i0 < nbat; i0 += kUT) {
+      const int i = i0 + tid;
+      int sz = 0;
+      if (i < nbat) {
+        const uint32_t bw = bat[i];
+        const int r0 = (int)(bw >> 8), m = (int)(bw & 0xff);
+        sz = rec_units(m, sm.rbeg[r0 + m] - sm.rbeg[r0]);
+      }
+      int tot;
+      const int ex = block_scan_excl<kUT>(sz, sm.wsum, &tot);
+      if (i < nbat) roff[i] = (uint32_t)(carry + ex);
+      carry += tot;
+    }
+    if (tid == 0) {
+      sm.hbase = nbat ? atomicAdd(&q.ctr[2], nbat) : 0;
+      const int rb = nbat ? atomicAdd(&q.ctr[3], carry) : 0;
+      sm.rbase16 = rb;
+      if ((int64_t)sm.hbase + nbat > q.hdr_cap || (int64_t)rb + carry > q.rec_cap) {
+        atomicExch(&q.ctr[4], 1);  // capacity bound violated: the row kernel traps
+        sm.nbat = 0;
+      }
+    }
+  }
   __syncthreads();
-  for (int i = tid; i < sm.nbat; i += kUT) {
+  const uint32_t rbase = (uint32_t)sm.rbase16;
+  for (int i = warp; i < sm.nbat; i += kUW) {
     const uint32_t bw = bat[i];
     const int r0 = (int)(bw >> 8), m = (int)(bw & 0xff);
-    const int e0 = sm.rbeg[r0], e1 = sm.rbeg[r0 + m];
-    uint4 h;
-    h.x = (uint32_t)(bs + rowidx0 + r0);   // first row record
-    h.y = (uint32_t)(bs + e0);             // first entry (sorted list in ent2)
-    h.z = (uint32_t)m | ((uint32_t)(e1 - e0) << 8);
-    h.w = (uint32_t)t;
-    q.hdr[sm.hbase + i] = h;
+    const int e0 = sm.rbeg[r0], nent = sm.rbeg[r0 + m] - e0;
+    const uint32_t o16 = rbase + roff[i];
+    uint32_t* rec = q.rec + (int64_t)o16 * 4;
+    if (lane == 0) {
+      rec[0] = (uint32_t)m | ((uint32_t)nent << 8);
+      rec[1] = (uint32_t)t;
+      q.hdr[sm.hbase + i] = make_uint2(o16, (uint32_t)rec_units(m, nent));
+    }
+    const int rw = 4 + 4 * ((m + 3) / 4);  // first length byte at word rw
+    if (lane < m) {
+      const int rs = sm.rbeg[r0 + lane];
+      rec[4 + lane] = (uint32_t)(c.row0 + (int64_t)(list[rs] >> c.bag_bits));
+      reinterpret_cast<uint8_t*>(rec + rw)[lane] = (uint8_t)(sm.rbeg[r0 + lane + 1] - rs);
+    }
+    uint32_t* bags = rec + rw + 4 * ((m + 15) / 16);
+    const int n4 = (nent + 3) & ~3;
+    for (int j = lane; j < n4; j += kWarp) bags[j] = list[e0 + min(j, nent - 1)] & c.bmask;
   }
+  __syncthreads();  // roff's buffer is reused for the long-row partials
   // long rows: every sub-warp of the CTA sums a contiguous piece, sub-warp 0
   // of warp 0 combines the pieces in order and applies the step
   int S = 1;
@@ -783,14 +837,6 @@ __global__ void __launch_bounds__(kUT, 2) bkt_sort_kernel(Params q, SegParams p)
       sort_pass(list, dst, n, q.bag_bits + k * wbits, nbits, sm);
       list = dst;
     }
-    // the row kernel reads the sorted list from ent2
-    if (list != q.ent2 + bs) {
-      for (int64_t i = tid; i < n; i += kUT) q.ent2[bs + i] = list[i];
-      if (!small) {
-        __syncthreads();
-        list = q.ent2 + bs;
-      }
-    }
     // row windows of <= kCap entries: heads compacted by a block scan
     int64_t pos = 0;
     int32_t rowidx0 = 0;
@@ -849,26 +895,38 @@ __global__ void __launch_bounds__(kUT, 2) bkt_sort_kernel(Params q, SegParams p)
 // (cp.async.bulk, completion counted in bytes on the stage's mbarrier), the
 // consumers sum each row's upstream rows in order and apply one step.
 
-constexpr int kRG = 4;    // groups per CTA
-constexpr int kRC = 3;    // consumer warps per group
-constexpr int kRS = 2;    // stages per group
+#ifndef NEO_BKT_RG
+#define NEO_BKT_RG 4
+#endif
+#ifndef NEO_BKT_RC
+#define NEO_BKT_RC 3
+#endif
+#ifndef NEO_BKT_RS
+#define NEO_BKT_RS 2
+#endif
+constexpr int kRG = NEO_BKT_RG;  // groups per CTA
+constexpr int kRC = NEO_BKT_RC;  // consumer warps per group
+constexpr int kRS = NEO_BKT_RS;  // stages per group
 constexpr int kRT = kRG * (1 + kRC) * kWarp;
+
+constexpr int kRQ = 3;  // record ring slots per group (records two batches ahead)
 
 struct StageMeta {
   int32_t m;       // rows (-1: end of stream)
   int32_t nent;
   int32_t t;
-  int32_t pad;
+  uint32_t mlo;    // row-wise state: first row of the staged moment span (~0u: read from HBM)
   uint32_t row[kMaxRows];
   uint16_t eoff[kMaxRows];
   uint8_t len[kMaxRows];
-  uint8_t mdir[kMaxRows];  // 1: moment read straight from global (chunk past the end)
 };
 
 struct RowSmem {
   uint64_t full[kRG][kRS];
   uint64_t empty[kRG][kRS];
+  uint64_t recbar[kRG][kRQ];
   StageMeta meta[kRG][kRS];
+  alignas(128) uint32_t rec[kRG][kRQ][kRecMax16 * 4];
   alignas(128) unsigned char data[kRG][kRS][kStageBytes];
 };
 
@@ -903,6 +961,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+// this thread's earlier cp.async copies complete the barrier's phase too
+__device__ __forceinline__ void mbar_arrive_cp(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+// four upstream rows (bags r0..r3, columns from col) -> consecutive smem rows
+__device__ __forceinline__ void gather4(void* dst, const CUtensorMap* map, int col, uint32_t r0, uint32_t r1,
+                                        uint32_t r2, uint32_t r3, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
@@ -919,9 +1001,22 @@ __device__ __forceinline__ void st16_hint(void* gmem, uint4 v, uint64_t pol) {
                : "memory");
 }
 
+// NEO_BKT_PROF builds: clock64 breakdown of the row kernel's roles
+// (diagnostics; read with neo_bkt_prof)
+#ifdef NEO_BKT_PROF
+__device__ unsigned long long g_bkt_prof[12];
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(k, x) \
+  if (lane == 0) atomicAdd(&g_bkt_prof[k], (unsigned long long)(x))
+#else
+#define PROF_T(v)
+#define PROF_ADD(k, x)
+#endif
+
 template <typename W, typename G, int OPT>
-__global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+__global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p,
+                                                          const __grid_constant__ CUtensorMap gmap, int32_t tma_dim) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];  // dynamic smem starts 1024-aligned
   RowSmem& sm = *reinterpret_cast<RowSmem*>(smem_raw);
   const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -929,59 +1024,84 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kRG; ++i)
       for (int s = 0; s < kRS; ++s) {
-        mbar_init(&sm.full[i][s], 1);
+        mbar_init(&sm.full[i][s], 1);  // producer lane 0 (arrive + expected bytes)
         mbar_init(&sm.empty[i][s], kRC);
       }
+    for (int i = 0; i < kRG; ++i)
+      for (int r = 0; r < kRQ; ++r) mbar_init(&sm.recbar[i][r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
   constexpr int kVW = 16 / (int)sizeof(W);  // W elements per 16-byte vector
   if (role == 0) {
     // ------------------------------------------------------------ producer
+    // Everything this warp moves goes through the TMA engine: per-lane global
+    // loads / cp.async stall a warp under this much memory traffic, TMA ops
+    // do not.  Per batch: the record (rows, lengths, bags) was bulk-copied
+    // into the record ring two batches ahead; upstream rows as tile::gather4
+    // ops (four rows each) or one bulk copy per row; weight rows (and
+    // element-wise state) as one bulk copy per run of consecutive rows; the
+    // row-wise moments as one 16-byte-aligned span.
+    if (q.ctr[4] != 0) __trap();  // the sort kernel overflowed a capacity bound
     const int64_t nhdr = q.ctr[2];
     const int64_t P = (int64_t)gridDim.x * kRG;
-    const uint32_t bmask = (uint32_t)((1u << q.bag_bits) - 1u);
     const G* gbase = reinterpret_cast<const G*>(p.grad);
+    const uint64_t pol_keep = policy_evict_last();
+    const uint64_t pol_first = policy_evict_first();
     int s = 0;
     uint32_t ephase = 1;  // stages start empty
-    // the weights stream through L2 once; the upstream rows of the table in
-    // flight are re-read by every occurrence and must stay resident
-    const uint64_t pol_stream = policy_evict_first();
-    const uint64_t pol_keep = policy_evict_last();
     int64_t i = (int64_t)blockIdx.x * kRG + g;
-    // batch i's header and records are in registers one iteration ahead
-    uint4 h = i < nhdr ? q.hdr[i] : make_uint4(0, 0, 0, 0);
-    uint32_t row_n = 0, bag_n[kMaxEnt / kWarp];
-    int len_n = 0;
-    auto load_batch = [&](const uint4& hh, bool ok) {
-      const int mm = (int)(hh.z & 0xff), ne = (int)(hh.z >> 8);
-      row_n = ok && lane < mm ? q.rrow[hh.x + lane] : 0u;
-      len_n = ok && lane < mm ? (int)q.rlen[hh.x + lane] : 0;
-#pragma unroll
-      for (int k = 0; k < kMaxEnt / kWarp; ++k) {
-        const int j = lane + k * kWarp;
-        bag_n[k] = ok && j < ne ? (q.ent2[hh.y + j] & bmask) : 0u;
+    auto hdr_at = [&](int64_t k) { return k < nhdr ? q.hdr[k] : make_uint2(0, 0); };
+    auto fetch_rec = [&](int slot, const uint2& hh, bool ok) {
+      if (ok && lane == 0) {
+        mbar_arrive_tx(&sm.recbar[g][slot], hh.y * 16);
+        bulk_g2s(sm.rec[g][slot], q.rec + (int64_t)hh.x * 4, hh.y * 16, &sm.recbar[g][slot], pol_first);
       }
     };
-    load_batch(h, i < nhdr);
-    uint4 hn = i + P < nhdr ? q.hdr[i + P] : make_uint4(0, 0, 0, 0);
+    uint2 hC = hdr_at(i + 2 * P);
+    fetch_rec(0, hdr_at(i), i < nhdr);
+    fetch_rec(1, hdr_at(i + P), i + P < nhdr);
+    int rs = 0;
+    uint32_t rph = 0;  // parity of the ring pass
+    int tcur = -1, D = 0, wb = 0, gb = 0;
+    int32_t doff = 0;
+    int64_t H = 0;
+    const W* wbase = nullptr;
+    const float* mbase = nullptr;
     for (; i < nhdr; i += P) {
-      const uint32_t row = row_n;
-      const int len = len_n;
-      uint32_t bag[kMaxEnt / kWarp];
+      PROF_T(p_top);
+      mbar_wait(&sm.recbar[g][rs], rph);
+      const uint32_t* rec = sm.rec[g][rs];
+      const int m = (int)(rec[0] & 0xff), nent = (int)(rec[0] >> 8), t = (int)rec[1];
+      const int rw = 4 + 4 * ((m + 3) / 4);
+      const uint32_t row = lane < m ? rec[4 + lane] : 0u;
+      const int len = lane < m ? (int)reinterpret_cast<const uint8_t*>(rec + rw)[lane] : 0;
+      const int ng = (nent + 3) >> 2;  // gather4 groups
+      const uint32_t* bg = rec + rw + 4 * ((m + 15) / 16);
+      uint4 b4 = lane < ng ? reinterpret_cast<const uint4*>(bg)[lane] : make_uint4(0, 0, 0, 0);
+      uint32_t bagx[3] = {0, 0, 0};  // per-entry path: entries lane, lane + 32, lane + 64
 #pragma unroll
-      for (int k = 0; k < kMaxEnt / kWarp; ++k) bag[k] = bag_n[k];
-      load_batch(hn, i + P < nhdr);  // next batch's records in flight while this one is issued
-      const uint4 hcur = h;
-      h = hn;
-      hn = i + 2 * P < nhdr ? q.hdr[i + 2 * P] : make_uint4(0, 0, 0, 0);
-      const int m = (int)(hcur.z & 0xff), nent = (int)(hcur.z >> 8), t = (int)hcur.w;
-      const int32_t doff = p.dim_offsets[t];
-      const int D = p.dim_offsets[t + 1] - doff;
-      const int64_t H = p.row_offsets[t + 1] - p.row_offsets[t];
-      const int wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
-      const int mb = OPT == NEO_OPT_ROWWISE_ADAGRAD ? 16 : (OPT == NEO_OPT_ADAGRAD ? D * 4 : 0);
-      const int gb = D * (int)sizeof(G);
+      for (int k = 0; k < 3; ++k)
+        if (lane + k * kWarp < nent) bagx[k] = bg[lane + k * kWarp];
+      __syncwarp();  // the slot is read: refill it with batch i + 2P
+      fetch_rec(rs == 0 ? 2 : rs - 1, hC, i + 2 * P < nhdr);
+      hC = hdr_at(i + 3 * P);
+      if (++rs == kRQ) {
+        rs = 0;
+        rph ^= 1;
+      }
+      if (t != tcur) {  // per-table constants (consecutive batches mostly share a table)
+        tcur = t;
+        doff = p.dim_offsets[t];
+        D = p.dim_offsets[t + 1] - doff;
+        H = p.row_offsets[t + 1] - p.row_offsets[t];
+        wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
+        gb = D * (int)sizeof(G);
+        if (OPT != NEO_OPT_NONE) wbase = reinterpret_cast<const W*>(p.weights[t]);
+        if (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD)
+          mbase = reinterpret_cast<const float*>(p.moments[t]);
+      }
+      const int mrb = OPT == NEO_OPT_ADAGRAD ? D * 4 : 0;  // element-wise state bytes per row
       int eoff = len;
 #pragma unroll
       for (int o = 1; o < kWarp; o <<= 1) {
@@ -989,43 +1109,77 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p)
         if (lane >= o) eoff += x;
       }
       eoff -= len;
-      const bool mdir = OPT == NEO_OPT_ROWWISE_ADAGRAD && (int64_t)(row | 3u) >= H;
-      const uint32_t mdv = __ballot_sync(full, lane < m && mdir);
+      // runs of consecutive rows (one bulk copy each)
+      const uint32_t prev = __shfl_up_sync(full, row, 1);
+      const bool start = lane < m && (lane == 0 || row != prev + 1u);
+      const unsigned starts = __ballot_sync(full, start);
+      int runlen = 0;
+      if (start) {
+        const unsigned later = starts & ~((2u << lane) - 1u);
+        runlen = (later ? __ffs(later) - 1 : m) - lane;
+      }
+      // row-wise moments: one 16-byte-aligned span when it is short and inside the table
+      uint32_t mlo = ~0u;
+      int mspan = 0;
+      if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
+        const uint32_t r0 = __shfl_sync(full, row, 0), r1 = __shfl_sync(full, row, m - 1);
+        const uint32_t lo = r0 & ~3u, hi = (r1 | 3u) + 1u;
+        if ((int64_t)hi <= H && (int)(hi - lo) * 4 <= kMomSpan) {
+          mlo = lo;
+          mspan = (int)(hi - lo) * 4;
+        }
+      }
+      const bool tma = D == tma_dim && (gb & 31) == 0;  // gather4 groups land 128-byte aligned
+      const uint32_t gbytes = (uint32_t)((tma ? ng * 4 : nent) * gb);
+      const uint32_t bytes = (uint32_t)(m * (wb + mrb) + mspan) + gbytes;
+      PROF_T(p_w0);
       mbar_wait(&sm.empty[g][s], ephase);
+      PROF_T(p_w1);
+      PROF_ADD(1, p_w1 - p_w0);
+      PROF_ADD(2, p_w0 - p_top);
       StageMeta& mt = sm.meta[g][s];
       if (lane < m) {
         mt.row[lane] = row;
         mt.eoff[lane] = (uint16_t)eoff;
         mt.len[lane] = (uint8_t)len;
-        mt.mdir[lane] = mdir ? 1 : 0;
       }
       if (lane == 0) {
         mt.m = m;
         mt.nent = nent;
         mt.t = t;
+        mt.mlo = mlo;
       }
-      __syncwarp();
-      const uint32_t bytes = (uint32_t)(m * wb + (m - __popc(mdv)) * mb + nent * gb);
-      if (lane == 0) mbar_arrive_tx(&sm.full[g][s], bytes);
       __syncwarp();
       unsigned char* st = sm.data[g][s];
       uint64_t* fb = &sm.full[g][s];
-      if (lane < m) {
-        if (OPT != NEO_OPT_NONE)
-          bulk_g2s(st + lane * wb, reinterpret_cast<const W*>(p.weights[t]) + (int64_t)row * D, wb, fb, pol_stream);
-        const float* mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD)
-                               ? reinterpret_cast<const float*>(p.moments[t])
-                               : nullptr;
-        if (OPT == NEO_OPT_ROWWISE_ADAGRAD && !mdir)
-          bulk_g2s(st + m * wb + lane * 16, mom + (row & ~3u), 16, fb, pol_stream);
-        if (OPT == NEO_OPT_ADAGRAD) bulk_g2s(st + m * wb + lane * mb, mom + (int64_t)row * D, mb, fb, pol_stream);
-      }
-      unsigned char* gst = st + ((m * (wb + mb) + 31) & ~31);
+      if (lane == 0) mbar_arrive_tx(fb, bytes);  // the phase completes when every byte has landed
+      __syncwarp();
+      unsigned char* gst = st + ((m * (wb + mrb) + mspan + 127) & ~127);
+      PROF_T(p_g0);
+      if (tma) {
+        if (lane < ng) gather4(gst + lane * 4 * gb, &gmap, doff, b4.x, b4.y, b4.z, b4.w, fb, pol_keep);
+      } else {
 #pragma unroll
-      for (int k = 0; k < kMaxEnt / kWarp; ++k) {
-        const int j = lane + k * kWarp;
-        if (j < nent) bulk_g2s(gst + j * gb, gbase + (int64_t)bag[k] * p.grad_stride + doff, gb, fb, pol_keep);
+        for (int k = 0; k < 3; ++k) {
+          const int j = lane + k * kWarp;
+          if (j < nent) bulk_g2s(gst + j * gb, gbase + (int64_t)bagx[k] * p.grad_stride + doff, gb, fb, pol_keep);
+        }
       }
+      PROF_T(p_g1);
+      PROF_ADD(8, p_g1 - p_g0);
+      if constexpr (OPT != NEO_OPT_NONE) {
+        if (start) {
+          bulk_g2s(st + lane * wb, wbase + (int64_t)row * D, runlen * wb, fb, pol_first);
+          if (OPT == NEO_OPT_ADAGRAD)
+            bulk_g2s(st + m * wb + lane * mrb, mbase + (int64_t)row * D, runlen * mrb, fb, pol_first);
+        }
+        if (OPT == NEO_OPT_ROWWISE_ADAGRAD && mspan && lane == 0)
+          bulk_g2s(st + m * wb, mbase + mlo, mspan, fb, pol_first);
+      }
+      PROF_T(p_end);
+      PROF_ADD(9, p_end - p_g1);
+      PROF_ADD(3, p_end - p_w1);
+      PROF_ADD(4, 1);
       if (++s == kRS) {
         s = 0;
         ephase ^= 1;
@@ -1052,14 +1206,21 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p)
   int s = 0;
   uint32_t fphase = 0;
   for (;;) {
+    PROF_T(c_w0);
     mbar_wait(&sm.full[g][s], fphase);
+    PROF_T(c_w1);
+    PROF_ADD(5, c_w1 - c_w0);
     const StageMeta& mt = sm.meta[g][s];
     const int m = mt.m;
     if (m < 0) break;
     const int t = mt.t;
     const int D = p.dim_offsets[t + 1] - p.dim_offsets[t];
     const int wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
-    const int mb = OPT == NEO_OPT_ROWWISE_ADAGRAD ? 16 : (OPT == NEO_OPT_ADAGRAD ? D * 4 : 0);
+    const int mb = OPT == NEO_OPT_ADAGRAD ? D * 4 : 0;  // element-wise state bytes per row
+    const uint32_t mlo = mt.mlo;
+    const int mspan = (OPT == NEO_OPT_ROWWISE_ADAGRAD && mlo != ~0u)
+                          ? (int)(((mt.row[m - 1] | 3u) + 1u - mlo) * 4)
+                          : 0;
     const int gb = D * (int)sizeof(G);
     const int nv = D / kVW;  // 16-byte W vectors per row
     int S = 1;
@@ -1067,7 +1228,7 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p)
     const int R = kWarp / S, sub = lane / S, sl = lane % S;
     const unsigned submask = S == kWarp ? full : (((1u << S) - 1u) << (sub * S));
     const unsigned char* st = sm.data[g][s];
-    const unsigned char* gst = st + ((m * (wb + mb) + 31) & ~31);
+    const unsigned char* gst = st + ((m * (wb + mb) + mspan + 127) & ~127);
     W* wt = reinterpret_cast<W*>(OPT == NEO_OPT_NONE ? p.dense_grads[t] : p.weights[t]);
     float* mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD) ? reinterpret_cast<float*>(p.moments[t])
                                                                            : nullptr;
@@ -1146,8 +1307,7 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p)
       if (!live) continue;
       float scale = lr;
       if (OPT == NEO_OPT_ROWWISE_ADAGRAD) {
-        const float mr = mt.mdir[rr] ? mom[row]
-                                     : reinterpret_cast<const float*>(st + m * wb + rr * 16)[row & 3u];
+        const float mr = mlo != ~0u ? reinterpret_cast<const float*>(st + m * wb)[row - mlo] : mom[row];
         const float mn = mr + ss * invD;
         if (sl == 0) mom[row] = mn;
         scale = __fdividef(lr, __fsqrt_rn(mn) + eps);
@@ -1180,6 +1340,9 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p)
       }
     }
     __syncwarp();
+    PROF_T(c_end);
+    PROF_ADD(6, c_end - c_w1);
+    PROF_ADD(7, 1);
     if (lane == 0) mbar_arrive(&sm.empty[g][s]);
     if (++s == kRS) {
       s = 0;
@@ -1212,6 +1375,36 @@ static int dbg(cudaStream_t s, const char* what) {
   return e == cudaSuccess ? NEO_OK : fail(NEO_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+template <typename G>
+static bool encode_gather_map(const SegParams& p, CUtensorMap* map) {
+  static EncodeTiledFn enc = [] {
+    EncodeTiledFn f = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&f, cudaEnableDefault, &qr) != cudaSuccess ||
+        qr != cudaDriverEntryPointSuccess)
+      return (EncodeTiledFn) nullptr;
+    return f;
+  }();
+  const char* off = std::getenv("NEO_BKT_NO_TMA");
+  if (!enc || (off && *off == '1') || p.max_dim < 8 || p.max_dim > 256 || (reinterpret_cast<uintptr_t>(p.grad) & 15) ||
+      ((p.grad_stride * sizeof(G)) & 15) || p.B > (int64_t(1) << 31))
+    return false;
+  const CUtensorMapDataType dt = sizeof(G) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : std::is_same<G, __half>::value ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                                  : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  cuuint64_t dims[2] = {(cuuint64_t)p.grad_stride, (cuuint64_t)p.B};
+  cuuint64_t strides[1] = {(cuuint64_t)p.grad_stride * sizeof(G)};
+  cuuint32_t box[2] = {(cuuint32_t)p.max_dim, 1};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, dt, 2, const_cast<void*>(p.grad), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 template <typename W, typename G, int OPT>
 static int launch_update(const Params& q, const SegParams& p, int sms, cudaStream_t s, bool prepare, bool apply) {
   if (prepare) {
@@ -1231,7 +1424,13 @@ static int launch_update(const Params& q, const SegParams& p, int sms, cudaStrea
     const int smem = (int)sizeof(RowSmem);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve row-kernel shared memory");
-    kern<<<(unsigned)sms, kRT, smem, s>>>(q, p);
+    // tile::gather4 tensor map over the upstream (B rows x grad_stride), box =
+    // one row of max_dim columns: tables of that width stage their upstream
+    // rows four per TMA op; other widths use 16-byte cp.async pieces
+    CUtensorMap gmap;
+    std::memset(&gmap, 0, sizeof(gmap));
+    const int32_t tma_dim = encode_gather_map<G>(p, &gmap) ? p.max_dim : 0;
+    kern<<<(unsigned)sms, kRT, smem, s>>>(q, p, gmap, tma_dim);
     return dbg(s, "neo_tbe_backward(bucket rows)");
   }
   return NEO_OK;
@@ -1260,12 +1459,33 @@ static int target_entries() {
 
 }  // namespace bkt
 
-size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows) {
+// capacity bounds of the batch stream (worst case over element types: f32
+// weights with element-wise state, f32 upstream).  In a 32-row chunk two
+// consecutive batches together overflow the stage budget or kMaxEnt (or the
+// first one ends at a long row), so batches <= 2 cost/budget + 2 N/kMaxEnt
+// + chunks + long rows; every batch has >= 1 row and every row >= 1 entry.
+static void stream_caps(int64_t N, int64_t nb, int32_t max_dim, int64_t* hdr_cap, int64_t* rec_cap) {
+  using namespace bkt;
+  const int64_t D = max_dim > 8 ? max_dim : 8;
+  const int64_t rowb = 8 * D, gb = 4 * D;
+  const int64_t budget = kStageBytes - 128 - kMomSpan - 3 * gb;
+  const int64_t lth = budget / gb - 3 > 1 ? budget / gb - 3 : 1;
+  const int64_t n = N > 0 ? N : 1;
+  const int64_t chunks = n / kWarp + nb + n / kCap + 1;
+  int64_t nbat = 2 * (n * (rowb + gb) / budget + 1) + 2 * (n / kMaxEnt + 1) + chunks + n / (lth + 1) + 64;
+  if (nbat > n + 64) nbat = n + 64;
+  *hdr_cap = nbat;
+  *rec_cap = 3 * nbat + n / 4 + n / 16 + n / 4 + 64;
+}
+
+size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows, int32_t max_dim) {
   using namespace bkt;
   const int64_t cpt = (B + kCHB - 1) / kCHB;
   const int64_t nb = bucket_bound(T, total_rows);
   const int64_t M = nb * cpt;
   const int64_t n1 = N > 0 ? N : 1;
+  int64_t hdr_cap, rec_cap;
+  stream_caps(N, nb, max_dim, &hdr_cap, &rec_cap);
   size_t b = 0;
   b += align256(sizeof(int32_t) * T);                    // sbits
   b += align256(sizeof(int64_t) * (T + 1));              // bbase
@@ -1273,11 +1493,10 @@ size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows) {
   b += align256(sizeof(int32_t) * (M / kScanTile + 2));  // scan tiles
   b += align256(sizeof(int32_t) * (nb + 1));             // bucket starts
   b += align256(sizeof(int32_t) * (nb + 1));             // big-bucket queue
-  b += align256(sizeof(int32_t) * 4);                    // counters
-  b += 2 * align256(sizeof(uint32_t) * n1);              // entries + sorted entries
-  b += align256(sizeof(uint32_t) * n1);                  // row records: row
-  b += align256(sizeof(uint8_t) * n1);                   // row records: length
-  b += align256(sizeof(uint4) * n1);                     // batch headers (<= one per entry)
+  b += align256(sizeof(int32_t) * 8);                    // counters
+  b += 2 * align256(sizeof(uint32_t) * n1);              // entries + big-bucket scratch
+  b += align256(sizeof(uint2) * hdr_cap);                // batch headers
+  b += align256((size_t)16 * rec_cap);                   // batch records
   return b;
 }
 
@@ -1306,7 +1525,7 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
                         int32_t index_dtype, void* workspace, size_t ws_bytes, neo_error* err, cudaStream_t s) {
   using namespace bkt;
   const int64_t N = p.N;
-  if (ws_bytes < bkt_workspace(p.T, p.B, N, p.total_rows))
+  if (ws_bytes < bkt_workspace(p.T, p.B, N, p.total_rows, p.max_dim))
     return fail(NEO_E_ARG, "neo_tbe_backward: workspace too small (bucketed path: neo_tbe_bucket_workspace_bytes)");
   Params q{};
   q.T = p.T;
@@ -1333,16 +1552,15 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
   q.big = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * (nb + 1));
   q.ctr = reinterpret_cast<int32_t*>(w);
-  w += align256(sizeof(int32_t) * 4);
+  w += align256(sizeof(int32_t) * 8);
   q.ent = reinterpret_cast<uint32_t*>(w);
   w += align256(sizeof(uint32_t) * n1);
   q.ent2 = reinterpret_cast<uint32_t*>(w);
   w += align256(sizeof(uint32_t) * n1);
-  q.rrow = reinterpret_cast<uint32_t*>(w);
-  w += align256(sizeof(uint32_t) * n1);
-  q.rlen = reinterpret_cast<uint8_t*>(w);
-  w += align256(sizeof(uint8_t) * n1);
-  q.hdr = reinterpret_cast<uint4*>(w);
+  stream_caps(N, nb, p.max_dim, &q.hdr_cap, &q.rec_cap);
+  q.hdr = reinterpret_cast<uint2*>(w);
+  w += align256(sizeof(uint2) * q.hdr_cap);
+  q.rec = reinterpret_cast<uint32_t*>(w);
 
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
@@ -1400,8 +1618,20 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
 
 }  // namespace neo
 
+#ifdef NEO_BKT_PROF
+extern "C" int neo_bkt_prof(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, neo::bkt::g_bkt_prof, sizeof(unsigned long long) * 12);
+  if (reset) {
+    unsigned long long z[12] = {0};
+    cudaMemcpyToSymbol(neo::bkt::g_bkt_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
+
 extern "C" size_t neo_tbe_bucket_workspace_bytes(int32_t num_tables, int64_t batch, int64_t num_indices,
-                                                 int64_t total_rows) {
-  if (num_tables < 0 || batch < 0 || num_indices < 0 || total_rows < 0) return 0;
-  return neo::bkt_workspace(num_tables, batch, num_indices, total_rows);
+                                                 int64_t total_rows, int32_t max_dim) {
+  if (num_tables < 0 || batch < 0 || num_indices < 0 || total_rows < 0 || max_dim < 0) return 0;
+  return neo::bkt_workspace(num_tables, batch, num_indices, total_rows, max_dim);
 }

@@ -222,7 +222,7 @@ class TableGroup:
             self._prepared = None
             mode_code |= capi.NEO_BWD_FLAG_DIM8
             n_b = n_idx if table_counts is None else int(sum(table_counts))
-            wsb = capi.lib().neo_tbe_bucket_workspace_bytes(self.T, batch, max(n_b, 1), self.total_rows)
+            wsb = capi.lib().neo_tbe_bucket_workspace_bytes(self.T, batch, max(n_b, 1), self.total_rows, self.max_dim)
             ws = WORKSPACE.get("tbe_bucket", wsb, self.device)
             if timers is None:
                 self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, lr, eps, pooling, err,
