@@ -56,8 +56,14 @@ constexpr int kMaxB = 2048;    // row buckets per table (count / scatter shared-
 constexpr int kSMin = 4;       // smallest bucket: 16 rows
 constexpr int kCHB = 2048;     // bags per count / scatter chunk
 constexpr int kScW = 8;        // warps per count / scatter CTA
-constexpr int kCap = 4096;     // entries per bucket sorted in shared memory
-constexpr int kUW = 16;        // warps per update CTA
+#ifndef NEO_BKT_CAP
+#define NEO_BKT_CAP 2048
+#endif
+#ifndef NEO_BKT_UW
+#define NEO_BKT_UW 8
+#endif
+constexpr int kCap = NEO_BKT_CAP;  // entries per bucket sorted in shared memory
+constexpr int kUW = NEO_BKT_UW;    // warps per sort CTA
 constexpr int kUT = kUW * kWarp;
 constexpr int kDigit = 9;      // bits per stable counting pass
 constexpr int kBins = 1 << kDigit;
@@ -66,7 +72,8 @@ constexpr int kEPL = 8;        // row elements per lane
 constexpr int kMaxDim = kWarp * kEPL;
 constexpr int kScanTile = 4096;  // 256 threads x 16
 constexpr int kTarget = 1024;    // default occurrences per bucket
-static_assert(kUT == kBins, "one digit bin per update thread");
+constexpr int kBPT = kBins / kUT;  // digit bins per sort thread
+static_assert(kBins % kUT == 0 && kCap % kUT == 0, "sort CTA geometry");
 static_assert(kBins * kUW * 2 >= kCap * 4, "batch list aliases the histograms");
 static_assert(kUW * kWarp * kEPL <= kCap, "long-row partials alias a sort buffer");
 
@@ -452,13 +459,24 @@ __device__ __forceinline__ void sort_pass(const uint32_t* src, uint32_t* dst, in
   const int tid = threadIdx.x;
   const int nbins = 1 << nbits;
   const uint32_t dm = (uint32_t)nbins - 1;
-  sm.tot[tid] = 0;  // kUT == kBins
+  for (int d = tid; d < kBins; d += kUT) sm.tot[d] = 0;
   __syncthreads();
   for (int64_t i = tid; i < n; i += kUT) atomicAdd(&sm.tot[(src[i] >> shift) & dm], 1);
   __syncthreads();
+  int v[kBPT], loc = 0;  // bins kBPT*tid .. : a local prefix, then one block scan
+#pragma unroll
+  for (int k = 0; k < kBPT; ++k) {
+    const int d = kBPT * tid + k;
+    v[k] = d < nbins ? sm.tot[d] : 0;
+    loc += v[k];
+  }
   int total;
-  const int ex = block_scan_excl<kUT>(tid < nbins ? sm.tot[tid] : 0, sm.wsum, &total);
-  sm.cursor[tid] = ex;
+  int ex = block_scan_excl<kUT>(loc, sm.wsum, &total);
+#pragma unroll
+  for (int k = 0; k < kBPT; ++k) {
+    sm.cursor[kBPT * tid + k] = ex;
+    ex += v[k];
+  }
   __syncthreads();
   for (int64_t c0 = 0; c0 < n; c0 += kCap) place_chunk(src, dst, c0, min64(n, c0 + kCap), shift, nbins, sm);
 }
@@ -507,10 +525,27 @@ __device__ __forceinline__ void st8(T* p, const float (&x)[kEPL]) {
 }
 
 // acc += upstream rows of entries [j0, j1) of list, in order; the trip count
-// (jmax - j0) is warp-uniform
-template <typename W, typename G, int OPT>
+// (jmax - j0) is warp-uniform.  KAHAN: compensated summation (hot rows, whose
+// thousands of terms would otherwise lose f32 accuracy to cancellation)
+template <typename W, typename G, int OPT, bool KAHAN = false>
 __device__ __forceinline__ void gather_sum(const RowCtx<W, G, OPT>& c, const uint32_t* list, int64_t j0, int64_t j1,
                                            int64_t jmax, bool col, int sl, float (&acc)[kEPL]) {
+  float comp[kEPL];
+#pragma unroll
+  for (int e = 0; e < kEPL; ++e) comp[e] = 0.f;
+  auto add = [&](const float (&x)[kEPL]) {
+#pragma unroll
+    for (int e = 0; e < kEPL; ++e) {
+      if (KAHAN) {
+        const float y = x[e] - comp[e];
+        const float t = acc[e] + y;
+        comp[e] = (t - acc[e]) - y;
+        acc[e] = t;
+      } else {
+        acc[e] += x[e];
+      }
+    }
+  };
   for (int64_t j = j0; j < jmax; j += 2) {
     const bool h0 = col && j < j1, h1 = col && j + 1 < j1;
     const uint32_t e0 = h0 ? list[j] : 0u;
@@ -518,14 +553,8 @@ __device__ __forceinline__ void gather_sum(const RowCtx<W, G, OPT>& c, const uin
     float x0[kEPL], x1[kEPL];
     if (h0) ld8<G>(c.grad + (int64_t)(e0 & c.bmask) * c.stride + c.doff + sl * kEPL, x0);
     if (h1) ld8<G>(c.grad + (int64_t)(e1 & c.bmask) * c.stride + c.doff + sl * kEPL, x1);
-    if (h0) {
-#pragma unroll
-      for (int e = 0; e < kEPL; ++e) acc[e] += x0[e];
-    }
-    if (h1) {
-#pragma unroll
-      for (int e = 0; e < kEPL; ++e) acc[e] += x1[e];
-    }
+    if (h0) add(x0);
+    if (h1) add(x1);
   }
 }
 
@@ -755,7 +784,7 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
     for (int e = 0; e < kEPL; ++e) acc[e] = 0.f;
     const int64_t a0 = rb + len * k / nsub, a1 = rb + len * (k + 1) / nsub;
     const int64_t span = (int64_t)__reduce_max_sync(full, (unsigned)(a1 - a0));
-    gather_sum<W, G, OPT>(c, list, a0, a1, a0 + span, col, sl, acc);
+    gather_sum<W, G, OPT, true>(c, list, a0, a1, a0 + span, col, sl, acc);
     if (col) {
 #pragma unroll
       for (int e = 0; e < kEPL; ++e) part[(k * S + sl) * kEPL + e] = acc[e];
@@ -779,7 +808,7 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
 }
 
 template <typename W, typename G, int OPT>
-__global__ void __launch_bounds__(kUT, 2) bkt_sort_kernel(Params q, SegParams p) {
+__global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, SegParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   USmem& sm = *reinterpret_cast<USmem*>(smem_raw);
   const int tid = threadIdx.x;
