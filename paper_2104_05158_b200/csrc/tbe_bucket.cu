@@ -90,9 +90,10 @@ struct Params {
   int32_t* mat;      // [nb*cpt + 1] counts, then exclusive offsets (+ total)
   int32_t* tiles;    // scan tile sums
   int32_t* bstart;   // [nb+1]
+  int32_t* btab;     // [nb] table of each bucket
   int32_t* big;      // queued big buckets
-  int32_t* ctr;      // [0] claim counter, [1] big-bucket count, [2] batches, [3] record units,
-                     // [4] capacity overflow
+  int32_t* ctr;      // [0] claim counter, [1] big-bucket count, [4] capacity overflow, [5] hot rows,
+                     // [6..7] one 64-bit counter: batches (low word), record units (high word)
   uint32_t* ent;     // bucketed entries (row_low << bag_bits | bag)
   uint32_t* ent2;    // bucket entries sorted by row (read by the row kernel)
   uint32_t* rec;     // row-batch records (16-byte units): {rows | entries << 8, table, -, -}, rows,
@@ -100,6 +101,8 @@ struct Params {
   uint2* hdr;        // per batch: {record offset, record size} in 16-byte units
   int64_t rec_cap;   // capacity of rec in 16-byte units
   int64_t hdr_cap;   // capacity of hdr
+  uint4* longs;      // hot rows: {table | sorted list in ent2 << 31, row, first entry, entries}
+  int64_t long_cap;
 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(256) bkt_classify_kernel(Params q) {
   const int32_t st = q.mat[b * q.cpt];
   const int32_t en = q.mat[(b + 1) * q.cpt];  // b + 1 == nbt: the total at mat[M]
   q.bstart[b] = st;
+  q.btab[b] = table_of_bucket(q.bbase, q.T, b);
   if (b + 1 == nbt) q.bstart[nbt] = en;
   if (en - st > kCap) q.big[atomicAdd(&q.ctr[1], 1)] = (int32_t)b;
 }
@@ -732,8 +736,13 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
       carry += tot;
     }
     if (tid == 0) {
-      sm.hbase = nbat ? atomicAdd(&q.ctr[2], nbat) : 0;
-      const int rb = nbat ? atomicAdd(&q.ctr[3], carry) : 0;
+      // one 64-bit reservation: batches (low word) and record units (high word)
+      const unsigned long long old =
+          nbat ? atomicAdd(reinterpret_cast<unsigned long long*>(q.ctr + 6),
+                           ((unsigned long long)carry << 32) | (unsigned long long)nbat)
+               : 0ull;
+      sm.hbase = (int)(old & 0xffffffffull);
+      const int rb = (int)(old >> 32);
       sm.rbase16 = rb;
       if ((int64_t)sm.hbase + nbat > q.hdr_cap || (int64_t)rb + carry > q.rec_cap) {
         atomicExch(&q.ctr[4], 1);  // capacity bound violated: the row kernel traps
@@ -765,24 +774,75 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
     for (int j = lane; j < n4; j += kWarp) bags[j] = list[e0 + min(j, nent - 1)] & c.bmask;
   }
   __syncthreads();  // roff's buffer is reused for the long-row partials
-  // long rows: every sub-warp of the CTA sums a contiguous piece, sub-warp 0
-  // of warp 0 combines the pieces in order and applies the step
-  int S = 1;
-  while (S * kEPL < c.D) S <<= 1;
-  const int R = kWarp / S, sub = lane / S, sl = lane % S;
-  const bool col = sl * kEPL < c.D;
+  // long rows are left to bkt_long_kernel (APPLY phase), so this kernel never
+  // touches the tables and may run under the forward: their sorted entries
+  // must be in global memory (ent2 for shared-memory lists)
   const int nl = sm.nlong;
-  const int nsub = kUW * R;
-  const int k = warp * R + sub;
-  float* part = reinterpret_cast<float*>(list == sm.a ? sm.b : sm.a);
-  for (int l = 0; l < nl; ++l) {
-    const int r = sm.longs[l];
-    const int64_t rb = sm.rbeg[r], re = sm.rbeg[r + 1], len = re - rb;
-    const int64_t row = c.row0 + (int64_t)(list[rb] >> c.bag_bits);
+  if (nl > 0) {
+    uint32_t buf = 1;
+    if (__isShared(list)) {
+      for (int i = tid; i < sm.rbeg[nr]; i += kUT) q.ent2[bs + i] = list[i];
+    } else {
+      buf = list == q.ent + bs ? 0u : 1u;
+    }
+    if (tid == 0) sm.hbase = atomicAdd(&q.ctr[5], nl);
+    __syncthreads();
+    const int lb = sm.hbase;
+    if ((int64_t)lb + nl > q.long_cap) {
+      if (tid == 0) atomicExch(&q.ctr[4], 1);
+    } else {
+      for (int l = tid; l < nl; l += kUT) {
+        const int r = sm.longs[l];
+        const int rb = sm.rbeg[r];
+        q.longs[lb + l] = make_uint4((uint32_t)t | (buf << 31), (uint32_t)(c.row0 + (int64_t)(list[rb] >> c.bag_bits)),
+                                     (uint32_t)(bs + rb), (uint32_t)(sm.rbeg[r + 1] - rb));
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// APPLY phase: one CTA per hot row (more occurrences than a row-kernel stage
+// holds).  Every sub-warp sums a contiguous piece of the row's sorted
+// occurrences with compensated summation; sub-warp 0 of warp 0 combines the
+// pieces in order and applies the row's single optimizer step.
+constexpr int kLW = 8;  // warps per long-row CTA
+
+template <typename W, typename G, int OPT>
+__global__ void __launch_bounds__(kLW* kWarp) bkt_long_kernel(Params q, SegParams p) {
+  __shared__ float part[kLW * kWarp * kEPL];
+  const unsigned full = 0xffffffffu;
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int nl = q.ctr[5];
+  for (int l = blockIdx.x; l < nl; l += gridDim.x) {
+    const uint4 rec = q.longs[l];
+    const int t = (int)(rec.x & 0x7fffffffu);
+    const uint32_t* list = ((rec.x >> 31) ? q.ent2 : q.ent) + rec.z;
+    const int64_t row = rec.y, len = rec.w;
+    RowCtx<W, G, OPT> c;
+    c.grad = reinterpret_cast<const G*>(p.grad);
+    c.stride = p.grad_stride;
+    c.doff = p.dim_offsets[t];
+    c.D = p.dim_offsets[t + 1] - c.doff;
+    c.wt = reinterpret_cast<W*>(OPT == NEO_OPT_NONE ? p.dense_grads[t] : p.weights[t]);
+    c.mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD) ? reinterpret_cast<float*>(p.moments[t])
+                                                                       : nullptr;
+    c.row0 = 0;
+    c.bag_bits = q.bag_bits;
+    c.bmask = (uint32_t)((1u << q.bag_bits) - 1u);
+    c.lr = (float)p.lr;
+    c.eps = (float)p.eps;
+    c.invD = 1.0f / (float)c.D;
+    int S = 1;
+    while (S * kEPL < c.D) S <<= 1;
+    const int R = kWarp / S, sub = lane / S, sl = lane % S;
+    const bool col = sl * kEPL < c.D;
+    const int nsub = kLW * R;
+    const int k = warp * R + sub;
     float acc[kEPL];
 #pragma unroll
     for (int e = 0; e < kEPL; ++e) acc[e] = 0.f;
-    const int64_t a0 = rb + len * k / nsub, a1 = rb + len * (k + 1) / nsub;
+    const int64_t a0 = len * k / nsub, a1 = len * (k + 1) / nsub;
     const int64_t span = (int64_t)__reduce_max_sync(full, (unsigned)(a1 - a0));
     gather_sum<W, G, OPT, true>(c, list, a0, a1, a0 + span, col, sl, acc);
     if (col) {
@@ -807,6 +867,78 @@ __device__ __forceinline__ void emit_rows(const RowCtx<W, G, OPT>& c, const Para
   }
 }
 
+// sort one bucket (entries in sm.a when it fits shared memory, else in
+// ent + bs) by row, then emit its row batches / hot rows window by window
+template <typename W, typename G, int OPT>
+__device__ __forceinline__ void sort_bucket(const Params& q, const SegParams& p, int b, int t, int64_t bs, int64_t n,
+                                            USmem& sm) {
+  const int tid = threadIdx.x;
+  const int s = q.sbits[t];
+  RowCtx<W, G, OPT> c;
+  c.doff = p.dim_offsets[t];
+  c.D = p.dim_offsets[t + 1] - c.doff;
+  c.row0 = (int64_t)(b - q.bbase[t]) << s;
+  c.bag_bits = q.bag_bits;
+  c.bmask = (uint32_t)((1u << q.bag_bits) - 1u);
+  // stable LSD passes over the s row bits (entries arrive in buffer order)
+  const int passes = (s + kDigit - 1) / kDigit;
+  const int wbits = (s + passes - 1) / passes;
+  const bool small = n <= kCap;
+  const uint32_t* list = small ? sm.a : q.ent + bs;
+  for (int k = 0; k < passes; ++k) {
+    const int nbits = min(wbits, s - k * wbits);
+    uint32_t* dst = small ? ((k & 1) ? sm.a : sm.b) : ((k & 1) ? q.ent + bs : q.ent2 + bs);
+    sort_pass(list, dst, n, q.bag_bits + k * wbits, nbits, sm);
+    list = dst;
+  }
+  // row windows of <= kCap entries: heads compacted by a block scan
+  int64_t pos = 0;
+  while (pos < n) {
+    const int64_t w1 = min64(n, pos + kCap);
+    constexpr int kPer = kCap / kUT;
+    const int64_t i0 = pos + (int64_t)tid * kPer;
+    unsigned hm = 0;
+    {
+      uint32_t prev = (i0 > pos && i0 < w1) ? (list[i0 - 1] >> q.bag_bits) : 0xffffffffu;
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const int64_t i = i0 + j;
+        if (i < w1) {
+          const uint32_t r = list[i] >> q.bag_bits;
+          if (r != prev) hm |= 1u << j;
+          prev = r;
+        }
+      }
+    }
+    int nr;
+    int ex = block_scan_excl<kUT>(__popc(hm), sm.wsum, &nr);
+#pragma unroll
+    for (int j = 0; j < kPer; ++j)
+      if ((hm >> j) & 1u) sm.rbeg[ex++] = (int32_t)(i0 + j - pos);
+    if (tid == 0) {
+      // end of the window's last row (it may run past the window)
+      int64_t end = w1;
+      if (w1 < n) {
+        const uint32_t last = list[w1 - 1] >> q.bag_bits;
+        int64_t lo = w1, hi = n;  // first index with a different (larger) row
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if ((list[mid] >> q.bag_bits) == last) lo = mid + 1;
+          else hi = mid;
+        }
+        end = lo;
+      }
+      sm.rbeg[nr] = (int32_t)(end - pos);
+      sm.nrows = nr;
+    }
+    __syncthreads();
+    const int nrw = sm.nrows;
+    emit_rows<W, G, OPT>(c, q, t, bs + pos, 0, list + pos, nrw, sm);
+    pos += sm.rbeg[nrw];
+    __syncthreads();
+  }
+}
+
 template <typename W, typename G, int OPT>
 __global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, SegParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -814,106 +946,79 @@ __global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, Seg
   const int tid = threadIdx.x;
   const int64_t nbt = q.bbase[q.T];
   const int nbig = q.ctr[1];
+  // 1. buckets larger than shared memory first (claimed; global passes); the
+  // first claim past the queue is this CTA's first regular bucket
+  int first = -1;
   for (;;) {
     if (tid == 0) {
-      int b = -1;
-      for (;;) {
-        const int idx = atomicAdd(&q.ctr[0], 1);
-        if (idx < nbig) {
-          b = q.big[idx];
-          break;
-        }
-        const int64_t j = (int64_t)idx - nbig;
-        if (j >= nbt) break;
-        const int n = q.bstart[j + 1] - q.bstart[j];
-        if (n > 0 && n <= kCap) {
-          b = (int)j;
-          break;
-        }
-      }
-      sm.bucket = b;
-      if (b >= 0) sm.table = table_of_bucket(q.bbase, q.T, b);
+      const int idx = atomicAdd(&q.ctr[0], 1);
+      sm.bucket = idx < nbig ? q.big[idx] : -1;
+      sm.table = idx - nbig;  // regular bucket index when past the queue
     }
     __syncthreads();
     const int b = sm.bucket;
-    if (b < 0) break;
-    const int t = sm.table;
-    const int s = q.sbits[t];
+    if (b < 0) {
+      first = sm.table;
+      break;
+    }
     const int64_t bs = q.bstart[b];
-    const int64_t n = q.bstart[b + 1] - bs;
-    RowCtx<W, G, OPT> c;
-    c.grad = reinterpret_cast<const G*>(p.grad);
-    c.stride = p.grad_stride;
-    c.doff = p.dim_offsets[t];
-    c.D = p.dim_offsets[t + 1] - c.doff;
-    c.wt = reinterpret_cast<W*>(OPT == NEO_OPT_NONE ? p.dense_grads[t] : p.weights[t]);
-    c.mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD) ? reinterpret_cast<float*>(p.moments[t])
-                                                                       : nullptr;
-    c.row0 = (int64_t)(b - q.bbase[t]) << s;
-    c.bag_bits = q.bag_bits;
-    c.bmask = (uint32_t)((1u << q.bag_bits) - 1u);
-    c.lr = (float)p.lr;
-    c.eps = (float)p.eps;
-    c.invD = 1.0f / (float)c.D;
-    // stable LSD passes over the s row bits (entries arrive in buffer order)
-    const int passes = (s + kDigit - 1) / kDigit;
-    const int wbits = (s + passes - 1) / passes;
-    const bool small = n <= kCap;
-    const uint32_t* list = q.ent + bs;
-    for (int k = 0; k < passes; ++k) {
-      const int nbits = min(wbits, s - k * wbits);
-      uint32_t* dst = small ? ((k & 1) ? sm.b : sm.a) : ((k & 1) ? q.ent + bs : q.ent2 + bs);
-      sort_pass(list, dst, n, q.bag_bits + k * wbits, nbits, sm);
-      list = dst;
+    sort_bucket<W, G, OPT>(q, p, b, q.btab[b], bs, q.bstart[b + 1] - bs, sm);
+  }
+  // 2. the others in claim order (table-major, so the row kernel's batch
+  // stream keeps each table's upstream slice L2-resident); the next bucket is
+  // claimed and its entries loaded into registers while this one is sorted
+  constexpr int kPer = kCap / kUT;
+  auto claim = [&]() -> int64_t {  // thread 0 only
+    for (;;) {
+      const int64_t jj = (int64_t)atomicAdd(&q.ctr[0], 1) - nbig;
+      if (jj >= nbt) return -1;
+      const int n = q.bstart[jj + 1] - q.bstart[jj];
+      if (n > 0 && n <= kCap) return jj;
     }
-    // row windows of <= kCap entries: heads compacted by a block scan
-    int64_t pos = 0;
-    int32_t rowidx0 = 0;
-    while (pos < n) {
-      const int64_t w1 = min64(n, pos + kCap);
-      constexpr int kPer = kCap / kUT;
-      const int64_t i0 = pos + (int64_t)tid * kPer;
-      unsigned hm = 0;
-      {
-        uint32_t prev = (i0 > pos && i0 < w1) ? (list[i0 - 1] >> q.bag_bits) : 0xffffffffu;
-#pragma unroll
-        for (int j = 0; j < kPer; ++j) {
-          const int64_t i = i0 + j;
-          if (i < w1) {
-            const uint32_t r = list[i] >> q.bag_bits;
-            if (r != prev) hm |= 1u << j;
-            prev = r;
-          }
-        }
-      }
-      int nr;
-      int ex = block_scan_excl<kUT>(__popc(hm), sm.wsum, &nr);
-#pragma unroll
-      for (int j = 0; j < kPer; ++j)
-        if ((hm >> j) & 1u) sm.rbeg[ex++] = (int32_t)(i0 + j - pos);
-      if (tid == 0) {
-        // end of the window's last row (it may run past the window)
-        int64_t end = w1;
-        if (w1 < n) {
-          const uint32_t last = list[w1 - 1] >> q.bag_bits;
-          int64_t lo = w1, hi = n;  // first index with a different (larger) row
-          while (lo < hi) {
-            const int64_t mid = (lo + hi) >> 1;
-            if ((list[mid] >> q.bag_bits) == last) lo = mid + 1;
-            else hi = mid;
-          }
-          end = lo;
-        }
-        sm.rbeg[nr] = (int32_t)(end - pos);
-        sm.nrows = nr;
-      }
-      __syncthreads();
-      const int nrw = sm.nrows;
-      emit_rows<W, G, OPT>(c, q, t, bs + pos, rowidx0 - (int32_t)pos, list + pos, nrw, sm);
-      rowidx0 += nrw;
-      pos += sm.rbeg[nrw];
-      __syncthreads();
+  };
+  if (tid == 0) {
+    int64_t jj = first;
+    if (jj >= nbt) {
+      jj = -1;
+    } else {
+      const int n = q.bstart[jj + 1] - q.bstart[jj];
+      if (n <= 0 || n > kCap) jj = claim();
     }
+    sm.bucket = (int)jj;
+  }
+  __syncthreads();
+  int64_t jn = sm.bucket;
+  int64_t bsn = 0;
+  int nn = 0, tn = 0;
+  uint32_t pre[kPer];
+  auto prefetch = [&]() {
+    if (jn >= 0) {
+      bsn = q.bstart[jn];
+      nn = (int)(q.bstart[jn + 1] - bsn);
+      tn = q.btab[jn];
+    } else {
+      nn = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = tid + k * kUT;
+      pre[k] = i < nn ? q.ent[bsn + i] : 0u;
+    }
+  };
+  prefetch();
+  while (jn >= 0) {
+    const int64_t j = jn, bs = bsn;
+    const int n = nn, t = tn;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int i = tid + k * kUT;
+      if (i < n) sm.a[i] = pre[k];
+    }
+    if (tid == 0) sm.bucket = (int)claim();
+    __syncthreads();
+    jn = sm.bucket;
+    prefetch();  // in flight during the sort below
+    sort_bucket<W, G, OPT>(q, p, (int)j, t, bs, n, sm);
   }
 }
 
@@ -1072,7 +1177,7 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p,
     // element-wise state) as one bulk copy per run of consecutive rows; the
     // row-wise moments as one 16-byte-aligned span.
     if (q.ctr[4] != 0) __trap();  // the sort kernel overflowed a capacity bound
-    const int64_t nhdr = q.ctr[2];
+    const int64_t nhdr = q.ctr[6];
     const int64_t P = (int64_t)gridDim.x * kRG;
     const G* gbase = reinterpret_cast<const G*>(p.grad);
     const uint64_t pol_keep = policy_evict_last();
@@ -1449,6 +1554,9 @@ static int launch_update(const Params& q, const SegParams& p, int sms, cudaStrea
     if (rc) return rc;
   }
   if (apply) {
+    bkt_long_kernel<W, G, OPT><<<(unsigned)(sms * 4), kLW * kWarp, 0, s>>>(q, p);
+    const int rc = dbg(s, "neo_tbe_backward(bucket hot rows)");
+    if (rc) return rc;
     auto kern = bkt_rows_kernel<W, G, OPT>;
     const int smem = (int)sizeof(RowSmem);
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -1521,11 +1629,13 @@ size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows, int32_
   b += align256(sizeof(int32_t) * (M + 1));              // count matrix
   b += align256(sizeof(int32_t) * (M / kScanTile + 2));  // scan tiles
   b += align256(sizeof(int32_t) * (nb + 1));             // bucket starts
+  b += align256(sizeof(int32_t) * (nb + 1));             // bucket tables
   b += align256(sizeof(int32_t) * (nb + 1));             // big-bucket queue
   b += align256(sizeof(int32_t) * 8);                    // counters
   b += 2 * align256(sizeof(uint32_t) * n1);              // entries + big-bucket scratch
   b += align256(sizeof(uint2) * hdr_cap);                // batch headers
   b += align256((size_t)16 * rec_cap);                   // batch records
+  b += align256(sizeof(uint4) * (n1 / 16 + 64));         // hot rows (> 16 occurrences each)
   return b;
 }
 
@@ -1578,6 +1688,8 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
   w += align256(sizeof(int32_t) * (M / kScanTile + 2));
   q.bstart = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * (nb + 1));
+  q.btab = reinterpret_cast<int32_t*>(w);
+  w += align256(sizeof(int32_t) * (nb + 1));
   q.big = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * (nb + 1));
   q.ctr = reinterpret_cast<int32_t*>(w);
@@ -1590,6 +1702,9 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
   q.hdr = reinterpret_cast<uint2*>(w);
   w += align256(sizeof(uint2) * q.hdr_cap);
   q.rec = reinterpret_cast<uint32_t*>(w);
+  w += align256((size_t)16 * q.rec_cap);
+  q.longs = reinterpret_cast<uint4*>(w);
+  q.long_cap = n1 / 16 + 64;
 
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);

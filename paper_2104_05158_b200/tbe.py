@@ -219,9 +219,26 @@ class TableGroup:
                     mode_code |= capi.NEO_BWD_FLAG_FULL_ROWS
         if self._bucketed(mode, batch, grad, stride, pooling, dense_grads):
             # hand-written bucketed sort + fused reduce/optimizer over the whole group
-            self._prepared = None
             mode_code |= capi.NEO_BWD_FLAG_DIM8
             n_b = n_idx if table_counts is None else int(sum(table_counts))
+            prep = getattr(self, "_prepared", None)
+            self._prepared = None
+            if (prep is not None and prep.get("bucketed") and mode == "update"
+                    and prep["key"] == (indices.data_ptr(), offsets.data_ptr(), batch, n_b)):
+                # the sort phase was issued by prepare_backward (side stream): APPLY only
+                main = torch.cuda.current_stream(self.device)
+                main.wait_event(prep["event"])
+                if timers is not None:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                self._backward_call(indices, offsets, batch, grad, stride, mode_code | capi.NEO_BWD_FLAG_APPLY,
+                                    optim, lr, eps, pooling, err, 0, self.T, None, None, None, None, dense_ptrs, n_b,
+                                    ws=prep["ws"])
+                if timers is not None:
+                    e1.record()
+                    timers.setdefault("apply", []).append((e0, e1, 0, self.T))
+                self._prep_side.wait_stream(main)  # the workspace is free again after APPLY
+                return None
             wsb = capi.lib().neo_tbe_bucket_workspace_bytes(self.T, batch, max(n_b, 1), self.total_rows, self.max_dim)
             ws = WORKSPACE.get("tbe_bucket", wsb, self.device)
             if timers is None:
@@ -305,7 +322,27 @@ class TableGroup:
         if not self._streamed(batch, stride, pooling) or self.total_rows < 1:
             return False
         if self._bucketed("update", batch, grad, stride, pooling):
-            return False  # the bucketed backward has no separate sort phase
+            # the bucketed sort phase (count, scan, stable scatter, per-bucket
+            # row sort, batch records) reads only the ids and writes only its
+            # workspace, so it may run under the forward on a side stream
+            n_b = int(sum(table_counts))
+            mode_code = capi.NEO_BWD_UPDATE | capi.NEO_BWD_FLAG_DIM8 | capi.NEO_BWD_FLAG_PREPARE
+            wsb = capi.lib().neo_tbe_bucket_workspace_bytes(self.T, batch, max(n_b, 1), self.total_rows, self.max_dim)
+            ws = WORKSPACE.get("tbe_bucket_prep", wsb, self.device)
+            main = torch.cuda.current_stream(self.device)
+            if getattr(self, "_prep_side", None) is None:
+                self._prep_side = torch.cuda.Stream(device=self.device)
+            side = self._prep_side
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                if n_b > 0:
+                    self._backward_call(indices, offsets, batch, grad, stride, mode_code, optim, 0.05, 0.0, pooling, err,
+                                        0, self.T, None, None, None, None, None, n_b, ws=ws)
+                ev = torch.cuda.Event()
+                ev.record(side)
+            self._prepared = {"key": (indices.data_ptr(), offsets.data_ptr(), batch, n_b), "event": ev, "ws": ws,
+                              "bucketed": True}
+            return True
         groups = self._sort_groups() if self.total_rows >= (1 << SORT_BITS) else [(0, self.T)]
         if len(groups) == 1 and not hasattr(self, "_group_meta"):
             self._group_meta = {}
