@@ -301,9 +301,15 @@ __global__ void __launch_bounds__(256) bkt_classify_kernel(Params q) {
 // ---------------------------------------------------------------------------
 // 5. stable scatter into buckets
 
+__device__ __forceinline__ void st_u32_keep(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;\n" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
 template <typename Idx>
 __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, const Idx* __restrict__ indices) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t pol_keep;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_keep));
   const int t = blockIdx.x / q.cpt, cc = blockIdx.x % q.cpt;
   if (t >= q.T) return;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -376,8 +382,11 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
         const uint32_t bk = valid ? (uint32_t)(id >> s) : 0xffffffffu;
         const unsigned peers = __match_any_sync(full, bk);
         if (valid) {
+          // a bucket's entries land over the warp's lifetime: keep partially
+          // written sectors in L2 (a partial-sector eviction costs a DRAM
+          // read-modify-write)
           const uint32_t pos = wh[bk] + __popc(peers & lanemask_lt());
-          q.ent[pos] = (((uint32_t)id & rmask) << q.bag_bits) | (uint32_t)(bw + k);
+          st_u32_keep(q.ent + pos, (((uint32_t)id & rmask) << q.bag_bits) | (uint32_t)(bw + k), pol_keep);
         }
         __syncwarp();
         if (valid && (peers >> lane) == 1u) wh[bk] += __popc(peers);
