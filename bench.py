@@ -64,7 +64,7 @@ def parse_args(argv=None):
                         "forward capped at this many CTAs per SM (0 = uncapped; -1 = off)")
     p.add_argument("--no-cache-bench", action="store_true", help="skip the software row-cache replay line")
     p.add_argument("--cpu-sample-batch", type=int, default=0,
-                   help="samples per table in one CPU-baseline sample (default: full batch)")
+                   help="samples per step of the sampled CPU reference step (default 4096 of the batch)")
     return p.parse_args(argv)
 
 
@@ -162,59 +162,175 @@ def bwd_bytes(U_list, N, D, B, e=4, i=4, o=8):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port of the reference numpy code) — checker only
+# CPU legs: the reference's own numpy implementation — checker / baseline only
+#
+# One CPU "step" is a BOUNDED SAMPLE of the config-2 step: all 64 tables x
+# `n` samples (L ids each), forward_pooled + fused_backward_update with
+# row-wise AdaGrad and the reference's ones upstream, timed end to end.  The
+# tables are spread over worker processes (one table-parallel process per
+# host core, memory permitting); the step time is the wall time until every
+# worker is done, so value = n / step time is measured, never extrapolated.
+# The reference itself is sequential (cli.py:549): its one-core rate is n /
+# (sum of the measured per-table times).  When oracle/_ref (a copy of the
+# reference package) is present the REAL neosim functions run ("reference");
+# otherwise the oracle's port of the same numpy primitives ("port").
+
+REF_DIR = ROOT / "oracle" / "_ref"
 
 
-def _cpu_worker(args):
-    table_seed, H, D, n, L, reps = args
-    from oracle import tbe_oracle as O
+def _ref_worker(conn, table_ids, H, D, L, seed):
+    """Worker process: holds its tables, runs sampled steps on request."""
+    use_ref = (REF_DIR / "neosim").is_dir()
+    if use_ref:
+        sys.path.insert(0, str(REF_DIR))
+        from neosim import embedding as E
+        from neosim import model as M
 
-    rng = np.random.default_rng(table_seed)
-    values = rng.standard_normal((H, D))
-    moment = np.zeros(H)
-    lengths = np.full(n, L, dtype=np.int64)
-    times = []
-    for r in range(reps):
-        idx = rng.integers(0, H, size=n * L, dtype=np.int64)
-        t0 = time.perf_counter()
-        O.np_forward_pooled(values, lengths, idx)
-        ids, g = O.np_backward_sort_aggregate(lengths, idx, np.ones((n, D)))
-        O.np_apply("rowwise_adagrad", values, moment, ids, g, LR, EPS)
-        times.append(time.perf_counter() - t0)
-    return times
+        specs = tuple(M.TableSpec(id=f"t{t}", num_rows=H, dim=D, avg_pooling=float(L)) for t in table_ids)
+        model = M.ModelSpec(tables=specs, bottom_mlp_layers=(), top_mlp_layers=(), local_batch=1,
+                            mflops_per_sample=1.0, interaction_flops_per_sample=0.0, dense_param_bytes=0)
+        cfg = E.OptimizerConfig(E.OptimizerKind.ROWWISE_ADAGRAD, LR, EPS)
+        tables = E.build_tables(model, cfg, seed=seed)
+    else:
+        from oracle import tbe_oracle as O
+
+        rng0 = np.random.default_rng(seed)
+        tables = [(rng0.standard_normal((H, D)), np.zeros(H)) for _ in table_ids]
+    conn.send(("ready", "reference" if use_ref else "port"))
+    while True:
+        msg = conn.recv()
+        if msg[0] == "stop":
+            return
+        _, step_seed, n = msg
+        times = []
+        if use_ref:
+            batch = M.gen_synthetic_batch(model, n, seed=step_seed)
+            ones = np.ones((n, D))
+            for k, tab in enumerate(tables):
+                lengths, idx = batch.table_slice(k)
+                t0 = time.perf_counter()
+                E.forward_pooled(tab, lengths, idx)
+                E.fused_backward_update(tab, lengths, idx, ones, cfg)
+                times.append(time.perf_counter() - t0)
+        else:
+            rng = np.random.default_rng(step_seed)
+            lengths = np.full(n, L, dtype=np.int64)
+            for values, moment in tables:
+                idx = rng.integers(0, H, size=n * L, dtype=np.int64)
+                t0 = time.perf_counter()
+                O.np_forward_pooled(values, lengths, idx)
+                ids, g = O.np_backward_sort_aggregate(lengths, idx, np.ones((n, D)))
+                O.np_apply("rowwise_adagrad", values, moment, ids, g, LR, EPS)
+                times.append(time.perf_counter() - t0)
+        conn.send(("done", times))
 
 
-def cpu_procs(H, D, n, L, limit=None) -> int:
-    per_proc = H * D * 8 + 3 * n * L * D * 8 + (1 << 29)
-    try:
-        import psutil
+class RefWorkers:
+    """Table-parallel worker processes over the host cores."""
 
-        avail = psutil.virtual_memory().available
-    except Exception:
-        avail = 16 << 30
-    cores = os.cpu_count() or 1
-    p = max(1, min(cores, int(avail * 0.7 // per_proc)))
-    return min(p, limit) if limit else p
-
-
-class CpuPool:
-    """Table-parallel pool: one reference-port table step per process."""
-
-    def __init__(self, procs):
+    def __init__(self, T, H, D, L, procs=None):
         import multiprocessing as mp
 
-        self.procs = procs
-        self.pool = mp.get_context("spawn").Pool(procs)
+        per_table = H * D * 8 + H * 8
+        try:
+            import psutil
 
-    def run(self, H, D, n, L, reps, seed0=0):
-        jobs = [(seed0 + k, H, D, n, L, reps) for k in range(self.procs)]
+            avail = psutil.virtual_memory().available
+        except Exception:
+            avail = 16 << 30
+        cores = os.cpu_count() or 1
+        if procs is None:
+            procs = max(1, min(cores, T, int(avail * 0.6 // (per_table * max(1, math.ceil(T / cores))))))
+        self.procs = procs
+        ctx = mp.get_context("spawn")
+        self.conns, self.ps = [], []
+        for w in range(procs):
+            mine = list(range(w, T, procs))
+            a, b = ctx.Pipe()
+            proc = ctx.Process(target=_ref_worker, args=(b, mine, H, D, L, 1000 + w), daemon=True)
+            proc.start()
+            self.conns.append(a)
+            self.ps.append(proc)
+        kinds = {c.recv()[1] for c in self.conns}
+        self.kind = kinds.pop()
+
+    def step(self, seed, n):
+        """Wall time of one sampled step over all tables and the per-table times."""
         t0 = time.perf_counter()
-        res = self.pool.map(_cpu_worker, jobs)
-        return res, time.perf_counter() - t0
+        for w, c in enumerate(self.conns):
+            c.send(("step", seed * 1000 + w, n))
+        per = [t for c in self.conns for t in c.recv()[1]]
+        return time.perf_counter() - t0, per
 
     def close(self):
-        self.pool.close()
-        self.pool.join()
+        for c in self.conns:
+            c.send(("stop",))
+        for p in self.ps:
+            p.join(timeout=30)
+
+
+def cpu_sample(a) -> int:
+    return a.cpu_sample_batch or 4096
+
+
+def cpu_baseline(a, T_total) -> dict:
+    """The reference's CPU step on a bounded sample (see above), 2 steps."""
+    n = cpu_sample(a)
+    wk = RefWorkers(T_total, a.rows, a.dim, a.pooling)
+    wk.step(1, n)  # warm-up
+    walls, per = [], []
+    for k in range(2):
+        w, pt = wk.step(2 + k, n)
+        walls.append(w)
+        per.append(sum(pt))
+    wk.close()
+    wall, one = float(np.mean(walls)), float(np.mean(per))
+    return {"value": n / wall, "unit": UNIT, "cores": wk.procs, "kind": wk.kind,
+            "sample": f"each step: all {T_total} tables x {n:,} of {a.batch:,} samples x {a.pooling} ids, "
+                      f"forward_pooled + fused_backward_update (row-wise AdaGrad, ones upstream), "
+                      f"{'neosim (oracle/_ref)' if wk.kind == 'reference' else 'oracle numpy port'}; "
+                      f"tables spread over {wk.procs} processes; wall time of the sampled step (not scaled)",
+            "ms_per_sample_step": 1e3 * wall, "one_core": {"value": n / one, "unit": UNIT, "cores": 1,
+                                                           "ms_per_sample_step": 1e3 * one,
+                                                           "how": "sum of the measured per-table times "
+                                                                  "(the reference runs tables sequentially)"},
+            "nproc": os.cpu_count()}
+
+
+def run_reference(a, rank, world):
+    """--impl reference: the reference's own CPU implementation of the step,
+    every table, on a bounded sample of the batch per step (measured wall
+    time per step, all host cores; rank 0 only)."""
+    if rank != 0:
+        return
+    n = cpu_sample(a)
+    wk = RefWorkers(a.tables, a.rows, a.dim, a.pooling)
+    for k in range(a.warmup):
+        wk.step(100 + k, n)
+    walls, ones = [], []
+    for k in range(a.steps):
+        w, pt = wk.step(1000 + k, n)
+        walls.append(w)
+        ones.append(sum(pt))
+    wk.close()
+    ms = 1e3 * float(np.mean(walls))
+    value = n / (ms / 1e3)
+    sample = (f"each step: all {a.tables} tables x {n:,} of {a.batch:,} samples x {a.pooling} ids "
+              f"(a bounded sample of the config-2 step), "
+              f"{'neosim forward_pooled + fused_backward_update from oracle/_ref' if wk.kind == 'reference' else 'oracle numpy port'}"
+              f", row-wise AdaGrad, ones upstream; tables spread over {wk.procs} processes; ms_per_step is the "
+              f"measured wall time of that sampled step")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": workload_name(a), "tables": a.tables, "rows": a.rows, "dim": a.dim,
+                       "batch_per_gpu": a.batch, "pooling": a.pooling, "cpu_sample_samples_per_step": n},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": wk.procs, "kind": wk.kind, "sample": sample,
+                             "one_core": {"value": n / float(np.mean(ones)), "unit": UNIT, "cores": 1,
+                                          "how": "sum of the measured per-table times"},
+                             "nproc": os.cpu_count()},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 def cache_replay_bench(dev, cpu: bool = True) -> dict:
@@ -261,54 +377,6 @@ def cache_replay_bench(dev, cpu: bool = True) -> dict:
         out["cpu_baseline"] = {"value": m / dt, "unit": "accesses/s", "cores": 1, "kind": "port",
                                "sample": f"first {m:,} accesses, oracle C port of cache.py access() (sequential)"}
     return out
-
-
-def cpu_baseline(a, T_total) -> dict:
-    n = a.cpu_sample_batch or a.batch
-    procs = cpu_procs(a.rows, a.dim, n, a.pooling, limit=T_total)
-    pool = CpuPool(procs)
-    res, _ = pool.run(a.rows, a.dim, n, a.pooling, 1)
-    pool.close()
-    t_table = max(r[0] for r in res)  # one table per process, in parallel
-    rounds = math.ceil(T_total / procs)
-    step_s = t_table * rounds * (a.batch / n)
-    return {"value": a.batch / step_s, "unit": UNIT, "cores": procs, "kind": "port",
-            "sample": f"{procs} of {T_total} tables (one per process), {n:,} samples x {a.pooling} ids each, "
-                      f"fwd+sort-aggregate+row-wise AdaGrad with the reference's numpy primitives "
-                      f"(oracle/tbe_oracle.py np_*); step time = max table time x {rounds} rounds"
-                      + (f" x {a.batch // n} batch scale" if n != a.batch else ""),
-            "table_s": t_table}
-
-
-def run_reference(a, rank, world):
-    """--impl reference: the reference's CPU implementation (oracle port),
-    all host cores, rank 0 only."""
-    if rank != 0:
-        return
-    n = a.cpu_sample_batch or max(a.batch // 8, 1)
-    procs = cpu_procs(a.rows, a.dim, n, a.pooling, limit=a.tables)
-    pool = CpuPool(procs)
-    rounds = math.ceil(a.tables / procs)
-    scale = a.batch / n
-    for _ in range(a.warmup):
-        pool.run(a.rows, a.dim, n, a.pooling, 1, seed0=100)
-    steps = []
-    for k in range(a.steps):
-        res, _ = pool.run(a.rows, a.dim, n, a.pooling, 1, seed0=1000 + k)
-        steps.append(max(r[0] for r in res) * rounds * scale)
-    pool.close()
-    ms = 1e3 * float(np.mean(steps))
-    value = a.batch * world / (ms / 1e3) if world > 1 else a.batch / (ms / 1e3)
-    sample = (f"per step: {procs} of {a.tables} tables in parallel (one per process), {n:,} samples x "
-              f"{a.pooling} ids each; step time scaled x{rounds} rounds x{scale:g} batch")
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": workload_name(a), "tables": a.tables, "rows": a.rows, "dim": a.dim,
-                       "batch_per_gpu": a.batch, "pooling": a.pooling},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
 
 
 # ---------------------------------------------------------------------------

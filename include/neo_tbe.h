@@ -208,6 +208,13 @@ int neo_lengths_to_offsets(int64_t n, const int64_t* lengths, int64_t* offsets /
                            void* workspace, size_t workspace_bytes, void* stream);
 size_t neo_scan_workspace_bytes(int64_t n);
 
+/* ---- id range check (model.py:344-348 CombinedBatch validation) -------
+ * Table t's ids (positions offsets[t*B] .. offsets[(t+1)*B]) must lie in
+ * [0, rows[t]) (rows: device int64 [T]); the first offending position, its
+ * value and table are recorded in err (IndexOutOfRange).  T <= 65535. */
+int neo_check_indices(int32_t num_tables, int64_t batch, const int64_t* rows, const int64_t* offsets,
+                      const void* indices, int32_t index_dtype, neo_error* err, void* stream);
+
 /* ---- row-wise bucketisation (comms.py:107-141) -------------------------
  * n bags with offsets[n+1] over indices; shard s owns rows
  * [shard_starts[s], shard_starts[s+1]) (k+1 host values, tiling [0,H)).

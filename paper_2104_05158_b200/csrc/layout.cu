@@ -204,6 +204,23 @@ __global__ void gather_blocks_kernel(int32_t n, const uint64_t* __restrict__ src
 // ---------------------------------------------------------------------------
 // casts
 
+// range check of a CombinedBatch's ids (model.py:344-348, embedding.py:144-146):
+// table t's ids (positions offsets[t*B] .. offsets[(t+1)*B]) must lie in
+// [0, rows[t]); the first offending position is recorded in err
+template <typename Idx>
+__global__ void check_indices_kernel(int32_t T, int64_t B, const int64_t* __restrict__ rows,
+                                     const int64_t* __restrict__ offsets, const Idx* __restrict__ ids,
+                                     neo_error* err) {
+  const int t = blockIdx.y;
+  const int64_t lo = offsets[(int64_t)t * B], hi = offsets[(int64_t)(t + 1) * B];
+  const int64_t H = rows[t];
+  for (int64_t p = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < hi;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = (int64_t)ids[p];
+    if (v < 0 || v >= H) record_bad_index(err, p);
+  }
+}
+
 template <typename S, typename D>
 __global__ void cast_kernel(int64_t n, const S* __restrict__ src, D* __restrict__ dst) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
@@ -394,6 +411,25 @@ int neo_copy_pieces(int64_t rows, const neo_piece* pieces, int32_t num_pieces, i
   else return fail(NEO_E_ARG, "copy_pieces: unsupported dtype pair");
 #undef NEO_PC
   return check_launch("copy_pieces");
+}
+
+int neo_check_indices(int32_t num_tables, int64_t batch, const int64_t* rows, const int64_t* offsets,
+                      const void* indices, int32_t index_dtype, neo_error* err, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (num_tables < 0 || batch < 0) return fail(NEO_E_ARG, "check_indices: negative size");
+  if (num_tables > 65535) return fail(NEO_E_ARG, "check_indices: more than 65535 tables in one call");
+  if (num_tables == 0 || batch == 0 || !err) return NEO_OK;
+  const dim3 grid(64, (unsigned)num_tables);
+  if (index_dtype == NEO_I32)
+    check_indices_kernel<int32_t><<<grid, 256, 0, s>>>(num_tables, batch, rows, offsets, (const int32_t*)indices,
+                                                       err);
+  else
+    check_indices_kernel<int64_t><<<grid, 256, 0, s>>>(num_tables, batch, rows, offsets, (const int64_t*)indices,
+                                                       err);
+  int rc = check_launch("check_indices");
+  if (rc) return rc;
+  launch_error_finalize(err, indices, index_dtype, offsets, batch, num_tables, s);
+  return check_launch("check_indices(finalize)");
 }
 
 int neo_gather_blocks(int32_t n, const uint64_t* src_ptrs, const int64_t* counts,

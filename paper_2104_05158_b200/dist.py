@@ -38,7 +38,7 @@ import numpy as np
 import torch
 
 from . import tbe
-from .errors import LayoutMismatch
+from .errors import IndexOutOfRange, LayoutMismatch
 from .plan import RankLayout, rank_layout
 
 
@@ -408,8 +408,13 @@ class ShardedEmbedding:
                 recv = torch.zeros(W, dtype=torch.int64, device=self.device)
                 per_shard = torch.zeros(0, dtype=torch.int64, device=self.device)
             pad = torch.zeros(Smax - nS, dtype=torch.int64, device=self.device)
-            cnts.append(torch.cat([st.sc["send_counts"], recv, per_shard, pad]))
+            cnts.append(torch.cat([st.sc["send_counts"], recv, per_shard, pad, st.cache["err"].buf]))
         host = torch.stack(cnts).cpu().numpy()  # the one host sync of the step
+        for st, h in zip(S, host):
+            pos, val, tab = (int(x) for x in h[-3:])
+            if pos != np.iinfo(np.int64).max:  # IndexOutOfRange before any table is touched
+                table = int(np.int32(tab & 0xFFFFFFFF))
+                raise IndexOutOfRange(self.model.tables[table].id if 0 <= table < self.T else "", val)
         for st, h in zip(S, host):
             nS = len(self.lay.owned[st.rank])
             st.sc["idx_in_splits"] = h[:W].tolist()
@@ -460,10 +465,7 @@ class ShardedEmbedding:
             if upstream_fn is not None:
                 g = upstream_fn(p)
             else:
-                g = self._buf(st, "ones", p.numel(), p.dtype)[:p.numel()].view_as(p)
-                if not st.cache.get("ones_ready") is g.data_ptr():
-                    g.fill_(1.0)
-                    st.cache["ones_ready"] = g.data_ptr()
+                g = self._ones_like(st, p)
             self._pack_grad(st, g)
         ev.start("bwd")
         handles = [self.comm.all_to_all(
@@ -534,6 +536,17 @@ class ShardedEmbedding:
         sc["tab_off"] = tab_off
         L_dev = bt[2] if len(bt) > 2 and bt[2] is not None else torch.from_numpy(lengths.reshape(-1)).to(dev)
         sc["L_dev"] = L_dev
+        # ids outside their table are caught here, before anything moves: the
+        # first bad position rides the step's one host read (_exchange_inputs)
+        err = st.cache.get("err")
+        if err is None:
+            err = tbe.ErrorRecord(dev)
+            st.cache["err"] = err
+            st.cache["rows_dev"] = torch.tensor([t.num_rows for t in self.model.tables], dtype=torch.int64,
+                                                device=dev)
+        err.reset()
+        if ids.numel():
+            tbe.check_indices(st.cache["rows_dev"], tbe.lengths_to_offsets(L_dev), ids, B, err)
         es = ids.element_size()
         rw = {}
         for t, bounds in lay.rw_bounds.items():  # bucketise this rank's block per row-wise table

@@ -644,6 +644,15 @@ def apply_row_updates(weight: torch.Tensor, moment: Optional[torch.Tensor], ids:
         "neo_apply_row_updates")
 
 
+def check_indices(rows: torch.Tensor, offsets: torch.Tensor, indices: torch.Tensor, batch: int,
+                  err: ErrorRecord) -> None:
+    """Record the first id outside [0, rows[t]) of every table (device int64
+    rows [T], offsets [T*batch+1]) in err (neo_check_indices); no sync."""
+    T = int(rows.numel())
+    capi.check(capi.lib().neo_check_indices(T, batch, rows.data_ptr(), offsets.data_ptr(), indices.data_ptr(),
+                                            INDEX_CODE[indices.dtype], err.ptr, _stream()), "neo_check_indices")
+
+
 def raise_if_bad(err: ErrorRecord, table_ids: Sequence[str]) -> None:
     """Raise the reference's IndexOutOfRange for the first bad id (syncs)."""
     r = err.read()

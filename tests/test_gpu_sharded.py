@@ -185,3 +185,37 @@ def test_quantized_alltoall_fp16_fwd_bf16_bwd(pkg):
             assert (np.abs(got - v) <= 1e-5 * (np.abs(v) + np.abs(v - full[t])) + 1e-6).all()
     # byte contract: fp16 payload is exactly half of fp32 (criterion 8, test_acceptance.py:318-343)
     assert engq.pooled_send_bytes(0) * 2 == eng32.pooled_send_bytes(0)
+
+
+@pytest.mark.parametrize("bad_table", [0, 1])
+def test_sharded_step_raises_index_out_of_range_before_any_update(pkg, bad_table):
+    """An id outside its table raises the reference's IndexOutOfRange (table
+    id, value) from ShardedEmbedding.step before any shard is touched
+    (model.py:344-348; forward_pooled / bucketize_rowwise raise, embedding.py:
+    144-146, comms.py:127-129) — for a table-wise and a row-wise table."""
+    from paper_2104_05158_b200 import dist, plan as P
+    from paper_2104_05158_b200.comms import _local_batches
+    from paper_2104_05158_b200.errors import IndexOutOfRange
+
+    W, B = 2, 64
+    specs = [pkg.TableSpec(id="tw", num_rows=500, dim=32, avg_pooling=4.0),
+             pkg.TableSpec(id="rw", num_rows=900, dim=32, avg_pooling=4.0)]
+    model = pkg.ModelSpec(tables=tuple(specs), local_batch=B)
+    plan = P.ShardingPlan(W, W, (
+        P.TableAssignment("tw", P.Scheme(P.SchemeKind.TABLE_WISE), (P.Shard(0),)),
+        P.TableAssignment("rw", P.Scheme(P.SchemeKind.ROW_WISE),
+                          (P.Shard(0, rows=(0, 450)), P.Shard(1, rows=(450, 900))))))
+    batch = pkg.gen_synthetic_batch(model, W * B, seed=5)
+    L = np.asarray(batch.lengths)
+    idx = np.asarray(batch.indices).copy()
+    tab_off = np.concatenate(([0], np.cumsum(L.sum(axis=1))))
+    bad_pos = int(tab_off[bad_table]) + 3
+    idx[bad_pos] = specs[bad_table].num_rows + 7
+    eng = dist.ShardedEmbedding(model, plan, dist.LocalComm(W), B, dtype=torch.float32, optim="sgd",
+                                index_dtype=torch.int64)
+    before = [w.clone() for slot in range(W) for _, w, _ in eng.shard_tensors(slot)]
+    with pytest.raises(IndexOutOfRange) as e:
+        eng.step(_local_batches(pkg.CombinedBatch(L, idx), W), lr=0.1)
+    assert e.value.table_id == specs[bad_table].id and e.value.index == specs[bad_table].num_rows + 7
+    after = [w for slot in range(W) for _, w, _ in eng.shard_tensors(slot)]
+    assert all(torch.equal(a, b) for a, b in zip(before, after))
