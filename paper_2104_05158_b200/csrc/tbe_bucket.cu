@@ -72,6 +72,7 @@ constexpr int kEPL = 8;        // row elements per lane
 constexpr int kMaxDim = kWarp * kEPL;
 constexpr int kScanTile = 4096;  // 256 threads x 16
 constexpr int kTarget = 1024;    // default occurrences per bucket
+constexpr int kWCap = 1280;      // entries of a bucket one warp sorts (bkt_wsort_kernel)
 constexpr int kBPT = kBins / kUT;  // digit bins per sort thread
 static_assert(kBins % kUT == 0 && kCap % kUT == 0, "sort CTA geometry");
 static_assert(kBins * kUW * 2 >= kCap * 4, "batch list aliases the histograms");
@@ -91,8 +92,11 @@ struct Params {
   int32_t* tiles;    // scan tile sums
   int32_t* bstart;   // [nb+1]
   int32_t* btab;     // [nb] table of each bucket
+  uint8_t* bkind;    // [nb] 0 empty, 1 warp-sorted, 2 CTA (shared memory), 3 CTA (global scratch)
+  int32_t* ctal;     // kind-2 buckets
   int32_t* big;      // queued big buckets
-  int32_t* ctr;      // [0] claim counter, [1] big-bucket count, [4] capacity overflow, [5] hot rows,
+  int32_t* ctr;      // [0] CTA claim counter, [1] big-bucket count, [2] kind-2 count, [3] warp claim
+                     // counter, [4] capacity overflow, [5] hot rows,
                      // [6..7] one 64-bit counter: batches (low word), record units (high word)
   uint32_t* ent;     // bucketed entries (row_low << bag_bits | bag)
   uint32_t* ent2;    // bucket entries sorted by row (read by the row kernel)
@@ -293,9 +297,15 @@ __global__ void __launch_bounds__(256) bkt_classify_kernel(Params q) {
   const int32_t st = q.mat[b * q.cpt];
   const int32_t en = q.mat[(b + 1) * q.cpt];  // b + 1 == nbt: the total at mat[M]
   q.bstart[b] = st;
-  q.btab[b] = table_of_bucket(q.bbase, q.T, b);
+  const int t = table_of_bucket(q.bbase, q.T, b);
+  q.btab[b] = t;
   if (b + 1 == nbt) q.bstart[nbt] = en;
-  if (en - st > kCap) q.big[atomicAdd(&q.ctr[1], 1)] = (int32_t)b;
+  const int n = en - st;
+  // 1: one warp sorts it (bkt_wsort_kernel); 2: a CTA, in shared memory; 3: a CTA, through global scratch
+  const uint8_t kind = n == 0 ? 0 : (n <= kWCap && q.sbits[t] <= kDigit) ? 1 : (n <= kCap ? 2 : 3);
+  q.bkind[b] = kind;
+  if (kind == 3) q.big[atomicAdd(&q.ctr[1], 1)] = (int32_t)b;
+  if (kind == 2) q.ctal[atomicAdd(&q.ctr[2], 1)] = (int32_t)b;
 }
 
 // ---------------------------------------------------------------------------
@@ -953,7 +963,6 @@ __global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, Seg
   extern __shared__ __align__(16) unsigned char smem_raw[];
   USmem& sm = *reinterpret_cast<USmem*>(smem_raw);
   const int tid = threadIdx.x;
-  const int64_t nbt = q.bbase[q.T];
   const int nbig = q.ctr[1];
   // 1. buckets larger than shared memory first (claimed; global passes); the
   // first claim past the queue is this CTA's first regular bucket
@@ -977,24 +986,13 @@ __global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, Seg
   // stream keeps each table's upstream slice L2-resident); the next bucket is
   // claimed and its entries loaded into registers while this one is sorted
   constexpr int kPer = kCap / kUT;
-  auto claim = [&]() -> int64_t {  // thread 0 only
-    for (;;) {
-      const int64_t jj = (int64_t)atomicAdd(&q.ctr[0], 1) - nbig;
-      if (jj >= nbt) return -1;
-      const int n = q.bstart[jj + 1] - q.bstart[jj];
-      if (n > 0 && n <= kCap) return jj;
-    }
+  const int ncta = q.ctr[2];
+  auto claim = [&]() -> int64_t {  // thread 0 only: the next kind-2 bucket
+    const int k = atomicAdd(&q.ctr[0], 1) - nbig;
+    return k < ncta ? q.ctal[k] : -1;
   };
-  if (tid == 0) {
-    int64_t jj = first;
-    if (jj >= nbt) {
-      jj = -1;
-    } else {
-      const int n = q.bstart[jj + 1] - q.bstart[jj];
-      if (n <= 0 || n > kCap) jj = claim();
-    }
-    sm.bucket = (int)jj;
-  }
+  __syncthreads();  // every thread has read sm.bucket / sm.table
+  if (tid == 0) sm.bucket = first < ncta ? q.ctal[first] : -1;
   __syncthreads();
   int64_t jn = sm.bucket;
   int64_t bsn = 0;
@@ -1029,6 +1027,236 @@ __global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, Seg
     prefetch();  // in flight during the sort below
     sort_bucket<W, G, OPT>(q, p, (int)j, t, bs, n, sm);
   }
+}
+
+// ---------------------------------------------------------------------------
+// 6b. warp-per-bucket sort: the common bucket (<= kWCap entries, <= 9 row
+// bits) is sorted by ONE warp with no block barriers: a warp-private digit
+// histogram (match_any-aggregated), one warp scan that also lists the
+// touched rows, a stable match_any placement into shared memory, greedy
+// batching of 32-row chunks from one prefix scan each, and the records.
+
+struct alignas(16) WSmem {
+  uint32_t in[kWCap];        // the bucket's entries (cp.async-staged, buffer order)
+  uint32_t out[kWCap];       // ... sorted by row
+  uint32_t hist[kBins];      // digit counts, then cursors; after the placement: the batches
+  uint16_t rstart[kBins + 2];
+};
+constexpr int kWW = 8;  // warps per CTA
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+template <typename W, typename G, int OPT>
+__global__ void __launch_bounds__(kWW* kWarp) bkt_wsort_kernel(Params q, SegParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const unsigned full = 0xffffffffu;
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  WSmem& sm = reinterpret_cast<WSmem*>(smem_raw)[warp];
+  const int64_t nbt = q.bbase[q.T];
+  const uint32_t bmask = (uint32_t)((1u << q.bag_bits) - 1u);
+  const unsigned lt = lanemask_lt();
+  const int bb = q.bag_bits;
+  auto claim = [&]() -> int64_t {
+    int64_t j = -1;
+    if (lane == 0) {
+      for (;;) {
+        const int64_t jj = atomicAdd(&q.ctr[3], 1);
+        if (jj >= nbt) break;
+        if (q.bkind[jj] == 1) {
+          j = jj;
+          break;
+        }
+      }
+    }
+    return __shfl_sync(full, j, 0);
+  };
+  auto stage = [&](int64_t j) {  // the bucket's entries -> sm.in, asynchronously
+    if (j < 0) return;
+    const int64_t b0 = q.bstart[j];
+    const int n = (int)(q.bstart[j + 1] - b0);
+    for (int i = lane; i < n; i += kWarp) cp_async4(&sm.in[i], q.ent + b0 + i);
+  };
+  int64_t j = claim();
+  stage(j);
+  while (j >= 0) {
+    const int64_t jn = claim();  // the next bucket, claimed early (its metadata loads overlap this one)
+    const int t = q.btab[j];
+    const int sb = q.sbits[t];
+    const int64_t bs = q.bstart[j];
+    const int n = (int)(q.bstart[j + 1] - bs);
+    const int nbins = 1 << sb;
+    const uint32_t dm = (uint32_t)nbins - 1;
+    const int32_t doff = p.dim_offsets[t];
+    const int D = p.dim_offsets[t + 1] - doff;
+    const int64_t row0 = (int64_t)(j - q.bbase[t]) << sb;
+    for (int d = lane; d < nbins; d += kWarp) sm.hist[d] = 0;
+    cp_async_wait_all();
+    __syncwarp();
+    // 1. digit histogram
+    for (int i0 = 0; i0 < n; i0 += kWarp) {
+      const int i = i0 + lane;
+      const bool v = i < n;
+      const uint32_t d = v ? (sm.in[i] >> bb) & dm : 0xffffffffu;
+      const unsigned peers = __match_any_sync(full, d);
+      if (v && (peers >> lane) == 1u) sm.hist[d] += (uint32_t)__popc(peers);
+      __syncwarp();
+    }
+    // 2. one scan: cursors (exclusive starts) and the touched rows in order
+    const int per = (nbins + kWarp - 1) / kWarp;
+    int cnt = 0, nz = 0;
+    for (int k = 0; k < per; ++k) {
+      const int d = lane * per + k;
+      const int c = d < nbins ? (int)sm.hist[d] : 0;
+      cnt += c;
+      nz += c > 0;
+    }
+    int ex = cnt, exn = nz;
+#pragma unroll
+    for (int o = 1; o < kWarp; o <<= 1) {
+      const int x = __shfl_up_sync(full, ex, o), y = __shfl_up_sync(full, exn, o);
+      if (lane >= o) {
+        ex += x;
+        exn += y;
+      }
+    }
+    const int nrows = __shfl_sync(full, exn, kWarp - 1);
+    ex -= cnt;
+    exn -= nz;
+    for (int k = 0; k < per; ++k) {
+      const int d = lane * per + k;
+      if (d < nbins) {
+        const int c = (int)sm.hist[d];
+        if (c > 0) sm.rstart[exn++] = (uint16_t)ex;
+        sm.hist[d] = (uint32_t)ex;
+        ex += c;
+      }
+    }
+    if (lane == 0) sm.rstart[nrows] = (uint16_t)n;
+    __syncwarp();
+    // 3. stable placement (entries arrive in buffer order)
+    for (int i0 = 0; i0 < n; i0 += kWarp) {
+      const int i = i0 + lane;
+      const bool v = i < n;
+      const uint32_t e = v ? sm.in[i] : 0u;
+      const uint32_t d = v ? (e >> bb) & dm : 0xffffffffu;
+      const unsigned peers = __match_any_sync(full, d);
+      if (v) sm.out[sm.hist[d] + __popc(peers & lt)] = e;
+      __syncwarp();
+      if (v && (peers >> lane) == 1u) sm.hist[d] += (uint32_t)__popc(peers);
+      __syncwarp();
+    }
+    stage(jn);  // sm.in is free: the next bucket's entries land during the emission below
+    // 4. batches of 32-row chunks (greedy cuts from one prefix scan per chunk);
+    // rows longer than a stage go to the hot-row list
+    uint32_t* bat = sm.hist;
+    const int lth = long_threshold<W, G, OPT>(D);
+    const int rowb = stage_row_bytes<W, G, OPT>(D);
+    const int gb = D * (int)sizeof(G);
+    const int lim = kStageBytes - stage_fixed_bytes<OPT>() - 3 * gb;
+    int nbat = 0;
+    for (int ck = 0; ck < nrows; ck += kWarp) {
+      const int r = ck + lane;
+      const bool v = r < nrows;
+      const int len = v ? sm.rstart[r + 1] - sm.rstart[r] : 0;
+      const bool lg = v && len > lth;
+      const unsigned lgm = __ballot_sync(full, lg);
+      if (lg) {  // hot row: its sorted entries to ent2, a record for bkt_long_kernel
+        const int l = atomicAdd(&q.ctr[5], 1);
+        if (l < q.long_cap)
+          q.longs[l] = make_uint4((uint32_t)t | (1u << 31),
+                                  (uint32_t)(row0 + ((sm.out[sm.rstart[r]] >> bb) & dm)),
+                                  (uint32_t)(bs + sm.rstart[r]), (uint32_t)len);
+        else
+          atomicExch(&q.ctr[4], 1);
+      }
+      for (unsigned h = lgm; h;) {
+        const int k = __ffs(h) - 1;
+        h &= h - 1;
+        const int a0 = sm.rstart[ck + k], a1 = sm.rstart[ck + k + 1];
+        for (int i = a0 + lane; i < a1; i += kWarp) q.ent2[bs + i] = sm.out[i];
+      }
+      int cost = v && !lg ? rowb + len * gb : 0;
+      int ent = v && !lg ? len : 0;
+#pragma unroll
+      for (int o = 1; o < kWarp; o <<= 1) {
+        const int x = __shfl_up_sync(full, cost, o), y = __shfl_up_sync(full, ent, o);
+        if (lane >= o) {
+          cost += x;
+          ent += y;
+        }
+      }
+      const int m_chunk = min(kWarp, nrows - ck);
+      int base = 0;
+      while (base < m_chunk) {
+        if ((lgm >> base) & 1u) {
+          ++base;
+          continue;
+        }
+        const unsigned after = lgm & ~((2u << base) - 1u);
+        const int stop = after ? __ffs(after) - 1 : m_chunk;  // the batch ends before the next hot row
+        const int c0 = base ? __shfl_sync(full, cost, base - 1) : 0;  // base is warp-uniform
+        const int e0 = base ? __shfl_sync(full, ent, base - 1) : 0;
+        const bool fits = lane >= base && lane < stop && cost - c0 <= lim && ent - e0 <= kMaxEnt;
+        const int m = __popc(__ballot_sync(full, fits));  // >= 1: a short row always fits
+        if (lane == 0) bat[nbat] = ((uint32_t)(ck + base) << 8) | (uint32_t)m;
+        ++nbat;
+        base += m;
+      }
+    }
+    __syncwarp();
+    // 5. records: sizes -> total (warp scans), one 64-bit reservation per bucket
+    int tot = 0;
+    for (int i0 = 0; i0 < nbat; i0 += kWarp) {
+      const int i = i0 + lane;
+      int sz = 0;
+      if (i < nbat) {
+        const uint32_t bw = bat[i];
+        const int r0 = (int)(bw >> 8), m = (int)(bw & 0xff);
+        sz = rec_units(m, sm.rstart[r0 + m] - sm.rstart[r0]);
+      }
+      tot += __reduce_add_sync(full, (unsigned)sz);
+    }
+    unsigned long long old = 0;
+    if (lane == 0 && nbat)
+      old = atomicAdd(reinterpret_cast<unsigned long long*>(q.ctr + 6),
+                      ((unsigned long long)tot << 32) | (unsigned long long)nbat);
+    old = __shfl_sync(full, old, 0);
+    const int hbase = (int)(old & 0xffffffffull);
+    uint32_t o16 = (uint32_t)(old >> 32);
+    if ((int64_t)hbase + nbat > q.hdr_cap || (int64_t)o16 + tot > q.rec_cap) {
+      if (lane == 0) atomicExch(&q.ctr[4], 1);
+      nbat = 0;
+    }
+    for (int i = 0; i < nbat; ++i) {
+      const uint32_t bw = bat[i];
+      const int r0 = (int)(bw >> 8), m = (int)(bw & 0xff);
+      const int e0 = sm.rstart[r0], nent = sm.rstart[r0 + m] - e0;
+      uint32_t* rec = q.rec + (int64_t)o16 * 4;
+      if (lane == 0) {
+        rec[0] = (uint32_t)m | ((uint32_t)nent << 8);
+        rec[1] = (uint32_t)t;
+        q.hdr[hbase + i] = make_uint2(o16, (uint32_t)rec_units(m, nent));
+      }
+      const int rw = 4 + 4 * ((m + 3) / 4);
+      if (lane < m) {
+        const int rs = sm.rstart[r0 + lane];
+        rec[4 + lane] = (uint32_t)(row0 + ((sm.out[rs] >> bb) & dm));
+        reinterpret_cast<uint8_t*>(rec + rw)[lane] = (uint8_t)(sm.rstart[r0 + lane + 1] - rs);
+      }
+      uint32_t* bags = rec + rw + 4 * ((m + 15) / 16);
+      const int n4 = (nent + 3) & ~3;
+      for (int jx = lane; jx < n4; jx += kWarp) bags[jx] = sm.out[e0 + min(jx, nent - 1)] & bmask;
+      o16 += (uint32_t)rec_units(m, nent);
+    }
+    __syncwarp();
+    j = jn;
+  }
+  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
@@ -1559,7 +1787,17 @@ static int launch_update(const Params& q, const SegParams& p, int sms, cudaStrea
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kUT, smem);
     if (per_sm < 1) per_sm = 1;
     kern<<<(unsigned)(sms * per_sm), kUT, smem, s>>>(q, p);
-    const int rc = dbg(s, "neo_tbe_backward(bucket sort)");
+    int rc = dbg(s, "neo_tbe_backward(bucket sort)");
+    if (rc) return rc;
+    auto wkern = bkt_wsort_kernel<W, G, OPT>;
+    const int wsmem = (int)(sizeof(WSmem) * kWW);
+    if (cudaFuncSetAttribute(wkern, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem) != cudaSuccess)
+      return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve warp-sort shared memory");
+    int wper = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, wkern, kWW * kWarp, wsmem);
+    if (wper < 1) wper = 1;
+    wkern<<<(unsigned)(sms * wper), kWW * kWarp, wsmem, s>>>(q, p);
+    rc = dbg(s, "neo_tbe_backward(bucket warp sort)");
     if (rc) return rc;
   }
   if (apply) {
@@ -1639,6 +1877,8 @@ size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows, int32_
   b += align256(sizeof(int32_t) * (M / kScanTile + 2));  // scan tiles
   b += align256(sizeof(int32_t) * (nb + 1));             // bucket starts
   b += align256(sizeof(int32_t) * (nb + 1));             // bucket tables
+  b += align256(sizeof(uint8_t) * (nb + 1));             // bucket kinds
+  b += align256(sizeof(int32_t) * (nb + 1));             // kind-2 list
   b += align256(sizeof(int32_t) * (nb + 1));             // big-bucket queue
   b += align256(sizeof(int32_t) * 8);                    // counters
   b += 2 * align256(sizeof(uint32_t) * n1);              // entries + big-bucket scratch
@@ -1698,6 +1938,10 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
   q.bstart = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * (nb + 1));
   q.btab = reinterpret_cast<int32_t*>(w);
+  w += align256(sizeof(int32_t) * (nb + 1));
+  q.bkind = reinterpret_cast<uint8_t*>(w);
+  w += align256(sizeof(uint8_t) * (nb + 1));
+  q.ctal = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * (nb + 1));
   q.big = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * (nb + 1));

@@ -47,16 +47,30 @@ from .plan import RankLayout, rank_layout
 
 
 class Comm:
-    """Collectives over the ranks this process drives (``ranks``)."""
+    """Collectives over the ranks this process drives (``ranks``).
+
+    Byte accounting (the reference's byte contract, comms.py:366-540):
+    ``sent[label][w]`` is what rank w sent to OTHER ranks through the
+    collectives labelled ``label`` ("lengths", "ids", "pooled", "grad");
+    ``reduced[label][w]`` the payload bytes rank w contributed to an
+    all-reduce (ring traffic is 2(W-1)/W of it, comms.py:433-439)."""
 
     world: int
     ranks: list
 
-    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False):  # pragma: no cover
+    def _count(self, table: str, label: str, rank: int, nbytes: int) -> None:
+        d = getattr(self, table, None)
+        if d is None:
+            d = {}
+            setattr(self, table, d)
+        d.setdefault(label, [0] * self.world)[rank] += int(nbytes)
+
+    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False,
+                   label: str = "other"):  # pragma: no cover
         """Returns a handle with .wait() when async_op (None otherwise)."""
         raise NotImplementedError
 
-    def all_reduce_sum(self, tensors) -> None:  # pragma: no cover
+    def all_reduce_sum(self, tensors, label: str = "other") -> None:  # pragma: no cover
         raise NotImplementedError
 
 
@@ -72,15 +86,18 @@ class NcclComm(Comm):
         self.ranks = [dist.get_rank(group)]
         self.bytes_sent = 0
 
-    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False):
+    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False, label: str = "other"):
         osp = [int(x) for x in out_splits[0]]
         isp = [int(x) for x in in_splits[0]]
         # persistent buffers may be larger than this step's payload
         out, inp = outs[0][:sum(osp)], ins[0][:sum(isp)]
-        self.bytes_sent += (sum(isp) - isp[self.ranks[0]]) * inp.element_size()
+        sent = (sum(isp) - isp[self.ranks[0]]) * inp.element_size()
+        self.bytes_sent += sent
+        self._count("sent", label, self.ranks[0], sent)
         return self.dist.all_to_all_single(out, inp, osp, isp, group=self.group, async_op=async_op)
 
-    def all_reduce_sum(self, tensors) -> None:
+    def all_reduce_sum(self, tensors, label: str = "other") -> None:
+        self._count("reduced", label, self.ranks[0], tensors[0].numel() * tensors[0].element_size())
         self.dist.all_reduce(tensors[0], group=self.group)
 
 
@@ -94,7 +111,7 @@ class LocalComm(Comm):
         self.ranks = list(range(world))
         self.bytes_sent = 0
 
-    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False):
+    def all_to_all(self, outs, ins, out_splits, in_splits, async_op: bool = False, label: str = "other"):
         W = self.world
         ioff = [np.concatenate(([0], np.cumsum(s)))[:-1] for s in in_splits]
         ooff = [np.concatenate(([0], np.cumsum(s)))[:-1] for s in out_splits]
@@ -107,8 +124,11 @@ class LocalComm(Comm):
                     outs[v][ooff[v][w]:ooff[v][w] + n].copy_(ins[w][ioff[w][v]:ioff[w][v] + n])
                     if v != w:
                         self.bytes_sent += n * ins[w].element_size()
+                        self._count("sent", label, w, n * ins[w].element_size())
 
-    def all_reduce_sum(self, tensors) -> None:
+    def all_reduce_sum(self, tensors, label: str = "other") -> None:
+        for w, t in enumerate(tensors):
+            self._count("reduced", label, w, t.numel() * t.element_size())
         acc = tensors[0].clone()
         for t in tensors[1:]:
             acc += t
@@ -395,7 +415,7 @@ class ShardedEmbedding:
             self._pack_lengths(st, bt)
         self.comm.all_to_all([st.sc["recv_len"] for st in S], [st.sc["send_len"] for st in S],
                              [[len(self.lay.owned[st.rank]) * B] * W for st in S],
-                             [[len(self.lay.owned[v]) * B for v in range(W)] for st in S])
+                             [[len(self.lay.owned[v]) * B for v in range(W)] for st in S], label="lengths")
         cnts = []
         Smax = max(len(self.lay.owned[st.rank]) for st in S)
         for st in S:
@@ -422,7 +442,7 @@ class ShardedEmbedding:
             st.sc["shard_counts"] = h[2 * W:2 * W + nS].tolist()
             self._pack_ids(st)
         self.comm.all_to_all([st.sc["recv_ids"] for st in S], [st.sc["send_ids"] for st in S],
-                             [st.sc["idx_out_splits"] for st in S], [st.sc["idx_in_splits"] for st in S])
+                             [st.sc["idx_out_splits"] for st in S], [st.sc["idx_in_splits"] for st in S], label="ids")
 
     def step(self, batches: Sequence, lr: float, eps: float = 0.0,
              upstream_fn: Optional[Callable] = None, timers: Optional[dict] = None):
@@ -439,7 +459,7 @@ class ShardedEmbedding:
         if self.transport == "nvlink":
             pooled = [self._step_nvlink(S[0], lr, eps, upstream_fn, ev)]
             if self.lay.dp_tables:
-                self.comm.all_reduce_sum([st.dp_dense for st in S])
+                self.comm.all_reduce_sum([st.dp_dense for st in S], label="dp")
                 for st in S:
                     self._dp_update(st, lr, eps)
             return pooled
@@ -453,7 +473,7 @@ class ShardedEmbedding:
             handles.append(self.comm.all_to_all(
                 [st.sc["recv_pool"][g] for st in S], [st.sc["send_pool"][g] for st in S],
                 [[B * self.gwidth[w][g] for w in range(W)] for st in S],
-                [[B * self.gwidth[st.rank][g]] * W for st in S], async_op=True))
+                [[B * self.gwidth[st.rank][g]] * W for st in S], async_op=True, label="pooled"))
         ev.stop("fwd")
         ev.start("a2a_fwd")
         for h in handles:
@@ -471,7 +491,8 @@ class ShardedEmbedding:
         handles = [self.comm.all_to_all(
             [st.sc["recv_grad"][g] for st in S], [st.sc["send_grad"][g] for st in S],
             [[B * self.gwidth[st.rank][g]] * W for st in S],
-            [[B * self.gwidth[v][g] for v in range(W)] for st in S], async_op=True) for g in range(self.G)]
+            [[B * self.gwidth[v][g] for v in range(W)] for st in S], async_op=True, label="grad")
+            for g in range(self.G)]
         for g, h in enumerate(handles):  # update of group g while group g+1's gradients arrive
             if h is not None:
                 h.wait()
@@ -481,7 +502,7 @@ class ShardedEmbedding:
             self._backward_dp(st)
         ev.stop("bwd")
         if self.lay.dp_tables:
-            self.comm.all_reduce_sum([st.dp_dense for st in S])
+            self.comm.all_reduce_sum([st.dp_dense for st in S], label="dp")
             for st in S:
                 self._dp_update(st, lr, eps)
         return pooled

@@ -211,8 +211,10 @@ def test_sharded_step_raises_index_out_of_range_before_any_update(pkg, bad_table
     tab_off = np.concatenate(([0], np.cumsum(L.sum(axis=1))))
     bad_pos = int(tab_off[bad_table]) + 3
     idx[bad_pos] = specs[bad_table].num_rows + 7
+    full = [torch.randn((t.num_rows, t.dim)) for t in specs]
     eng = dist.ShardedEmbedding(model, plan, dist.LocalComm(W), B, dtype=torch.float32, optim="sgd",
-                                index_dtype=torch.int64)
+                                index_dtype=torch.int64,
+                                init=lambda t, r, c: full[t][r[0]:r[1], c[0]:c[1]].contiguous())
     before = [w.clone() for slot in range(W) for _, w, _ in eng.shard_tensors(slot)]
     with pytest.raises(IndexOutOfRange) as e:
         eng.step(_local_batches(pkg.CombinedBatch(L, idx), W), lr=0.1)
