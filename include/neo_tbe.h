@@ -273,7 +273,7 @@ int neo_gather_blocks(int32_t n, const uint64_t* src_ptrs, const int64_t* counts
  * receive access p's AccessResult; stats[0..2] (device int64) = hits,
  * misses, evictions (cache.py:117-126 TraceStats).  A negative row is
  * recorded in err (first position); the reference raises InvalidValue
- * ("row_id") there.  ways <= 32 (one way per lane).  Replaces
+ * ("row_id") there.  ways <= 128 (up to four ways per lane).  Replaces
  * neosim.cache.simulate_trace / access over a trace. */
 enum { NEO_CACHE_LRU = 0, NEO_CACHE_LFU = 1 };
 size_t neo_cache_workspace_bytes(int64_t num_accesses);

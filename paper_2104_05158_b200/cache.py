@@ -81,8 +81,8 @@ def access_trace(config, trace, with_results: bool = True, device=None):
     once per element on a new CacheState (cache.py:68-98)."""
     from .tbe import WORKSPACE, ErrorRecord, _stream
 
-    if config.ways > 32:
-        raise InvalidValue("ways", "this implementation holds one way per lane (ways <= 32)")
+    if config.ways > 128:
+        raise InvalidValue("ways", "this implementation holds up to four ways per lane (ways <= 128)")
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     tr = trace if isinstance(trace, torch.Tensor) else torch.as_tensor(np.asarray(list(trace) if not isinstance(
         trace, np.ndarray) else trace, dtype=np.int64))

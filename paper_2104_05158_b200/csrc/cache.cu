@@ -43,6 +43,8 @@ struct CacheHead {
   __device__ __forceinline__ bool operator()(const int32_t& i) const { return i == 0 || keys[i] != keys[i - 1]; }
 };
 
+// K ways per lane: way k*32 + lane lives in lane `lane`, slot k (ways <= 32K)
+template <int K>
 __global__ void __launch_bounds__(256)
 cache_replay_kernel(const int64_t* __restrict__ trace, const int32_t* __restrict__ pos,
                     const int32_t* __restrict__ starts, const int64_t* __restrict__ num_segs, int64_t n,
@@ -53,16 +55,37 @@ cache_replay_kernel(const int64_t* __restrict__ trace, const int32_t* __restrict
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / kWarp;
   const int64_t S = *num_segs;
-  const unsigned waymask = ways >= 32 ? full : ((1u << ways) - 1u);
+  unsigned waymask[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int w = ways - k * kWarp;
+    waymask[k] = w >= 32 ? full : (w <= 0 ? 0u : ((1u << w) - 1u));
+  }
   unsigned long long h = 0, m = 0, e = 0;
   for (int64_t seg = warp; seg < S; seg += nwarps) {
     const int64_t s0 = starts[seg];
     const int64_t s1 = seg + 1 < S ? (int64_t)starts[seg + 1] : n;
-    int64_t row = -1;          // this lane's way
-    uint32_t last = 0, freq = 0;
-    bool valid = false;
+    int64_t row[K];            // this lane's ways
+    uint32_t last[K], freq[K];
+    bool valid[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      row[k] = -1;
+      last[k] = freq[k] = 0;
+      valid[k] = false;
+    }
     int cnt = 0;
     int64_t prev_r = -1;  // row of the set's previous access (resident after it)
+    // the (slot, lane) holding row r, as slot * 32 + lane, or -1
+    auto find = [&](int64_t r) -> int {
+      int where = -1;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const unsigned hm = __ballot_sync(full, valid[k] && row[k] == r);
+        if (where < 0 && hm) where = k * kWarp + __ffs(hm) - 1;
+      }
+      return where;
+    };
     for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
       const int mm = (int)min64(kWarp, s1 - j0);
       const int32_t my_p = lane < mm ? pos[j0 + lane] : 0;
@@ -81,11 +104,13 @@ cache_replay_kernel(const int64_t* __restrict__ trace, const int32_t* __restrict
           const int L = min(rest ? __ffs(rest) - 1 : kWarp - k, mm - k);
           const int64_t r = __shfl_sync(full, my_r, k);
           const uint32_t clock_end = (uint32_t)__shfl_sync(full, my_p, k + L - 1) + 1u;
-          const unsigned hm = __ballot_sync(full, valid && row == r);
-          if (lane == __ffs(hm) - 1) {
-            last = clock_end;
-            freq += (uint32_t)L;
-          }
+          const int wh = find(r);
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (wh == q * kWarp + lane) {
+              last[q] = clock_end;
+              freq[q] += (uint32_t)L;
+            }
           if (lane >= k && lane < k + L) {
             if (hit_out) hit_out[my_p] = 1;
             if (ev_out) ev_out[my_p] = -1;
@@ -98,12 +123,14 @@ cache_replay_kernel(const int64_t* __restrict__ trace, const int32_t* __restrict
         const int64_t r = __shfl_sync(full, my_r, k);
         const uint32_t clock = (uint32_t)p + 1u;
         ++k;
-        const unsigned hm = __ballot_sync(full, valid && row == r);
-        if (hm) {
-          if (lane == __ffs(hm) - 1) {
-            last = clock;
-            freq += 1;
-          }
+        const int wh = find(r);
+        if (wh >= 0) {
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (wh == q * kWarp + lane) {
+              last[q] = clock;
+              freq[q] += 1;
+            }
           ++h;
           if (lane == 0) {
             if (hit_out) hit_out[p] = 1;
@@ -113,27 +140,49 @@ cache_replay_kernel(const int64_t* __restrict__ trace, const int32_t* __restrict
         }
         ++m;
         int64_t ev = -1;
-        int tgt;
-        if (cnt < ways) {
-          tgt = __ffs(~__ballot_sync(full, valid) & waymask) - 1;
-          ++cnt;
-        } else {
-          uint32_t key = valid ? last : UINT_MAX;
-          if (lfu) {
-            const uint32_t fmin = __reduce_min_sync(full, valid ? freq : UINT_MAX);
-            key = (valid && freq == fmin) ? last : UINT_MAX;
+        int tgt = -1;
+        if (cnt < ways) {  // a free way (which one does not change any result)
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            const unsigned fm = ~__ballot_sync(full, valid[q]) & waymask[q];
+            if (tgt < 0 && fm) tgt = q * kWarp + __ffs(fm) - 1;
           }
-          const uint32_t lmin = __reduce_min_sync(full, key);
-          tgt = __ffs(__ballot_sync(full, valid && last == lmin)) - 1;
-          ev = __shfl_sync(full, row, tgt);
+          ++cnt;
+        } else {  // LRU: least recently used; LFU: least frequently used, then least recently
+          uint32_t fmin = UINT_MAX;
+          if (lfu) {
+            uint32_t f = UINT_MAX;
+#pragma unroll
+            for (int q = 0; q < K; ++q) f = min(f, valid[q] ? freq[q] : UINT_MAX);
+            fmin = __reduce_min_sync(full, f);
+          }
+          uint32_t key[K], kmin = UINT_MAX;
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            key[q] = (valid[q] && (!lfu || freq[q] == fmin)) ? last[q] : UINT_MAX;
+            kmin = min(kmin, key[q]);
+          }
+          const uint32_t lmin = __reduce_min_sync(full, kmin);
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            const unsigned bm = __ballot_sync(full, valid[q] && key[q] == lmin);
+            if (tgt < 0 && bm) tgt = q * kWarp + __ffs(bm) - 1;
+          }
+          int64_t evr = -1;
+#pragma unroll
+          for (int q = 0; q < K; ++q)
+            if (tgt / kWarp == q) evr = row[q];
+          ev = __shfl_sync(full, evr, tgt % kWarp);
           ++e;
         }
-        if (lane == tgt) {
-          row = r;
-          last = clock;
-          freq = 1;
-          valid = true;
-        }
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          if (tgt == q * kWarp + lane) {
+            row[q] = r;
+            last[q] = clock;
+            freq[q] = 1;
+            valid[q] = true;
+          }
         if (lane == 0) {
           if (hit_out) hit_out[p] = 0;
           if (ev_out) ev_out[p] = ev;
@@ -175,7 +224,7 @@ extern "C" int neo_cache_simulate(int64_t num_sets, int32_t ways, int32_t policy
   cudaStream_t s = as_stream(stream);
   if (num_sets < 1) return fail(NEO_E_ARG, "num_sets: must be >= 1");
   if (ways < 1) return fail(NEO_E_ARG, "ways: must be >= 1");
-  if (ways > kWarp) return fail(NEO_E_ARG, "ways: this implementation holds one way per lane (<= 32)");
+  if (ways > 4 * kWarp) return fail(NEO_E_ARG, "ways: this implementation holds up to 4 ways per lane (<= 128)");
   if (num_sets > (int64_t)UINT32_MAX) return fail(NEO_E_ARG, "num_sets: must be < 2^32");
   if (policy != NEO_CACHE_LRU && policy != NEO_CACHE_LFU) return fail(NEO_E_ARG, "policy: LRU or LFU");
   if (num_accesses < 0 || num_accesses >= INT_MAX) return fail(NEO_E_ARG, "trace: 0 .. 2^31-1 accesses");
@@ -212,9 +261,14 @@ extern "C" int neo_cache_simulate(int64_t num_sets, int32_t ways, int32_t policy
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t want = (min64(n, (int64_t)num_sets) + 7) / 8;
   const unsigned grid = (unsigned)(want < (int64_t)sms * 8 ? (want > 0 ? want : 1) : (int64_t)sms * 8);
-  cache_replay_kernel<<<grid, 256, 0, s>>>(trace, vbuf.Current(), starts, nseg, n, ways,
-                                           policy == NEO_CACHE_LFU ? 1 : 0, hit, evicted,
-                                           reinterpret_cast<unsigned long long*>(stats));
+  const int lfu = policy == NEO_CACHE_LFU ? 1 : 0;
+  unsigned long long* st = reinterpret_cast<unsigned long long*>(stats);
+  if (ways <= kWarp)
+    cache_replay_kernel<1><<<grid, 256, 0, s>>>(trace, vbuf.Current(), starts, nseg, n, ways, lfu, hit, evicted, st);
+  else if (ways <= 2 * kWarp)
+    cache_replay_kernel<2><<<grid, 256, 0, s>>>(trace, vbuf.Current(), starts, nseg, n, ways, lfu, hit, evicted, st);
+  else
+    cache_replay_kernel<4><<<grid, 256, 0, s>>>(trace, vbuf.Current(), starts, nseg, n, ways, lfu, hit, evicted, st);
   rc = check_launch("neo_cache_simulate(replay)");
   if (rc) return rc;
   return NEO_OK;

@@ -362,12 +362,28 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
     }
   }
   __syncthreads();
-  // place in buffer order: 32 bags per window, each lane finds its entry's
-  // bag by a shuffle search; ids of four rounds are loaded ahead
+  // place in buffer order, 32 bags per window
+  auto place = [&](int64_t p, bool in, int64_t id, uint32_t bag) {
+    const bool valid = in && id >= 0 && id < H;
+    const uint32_t bk = valid ? (uint32_t)(id >> s) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(full, bk);
+    if (valid) {
+      // a bucket's entries land over the warp's lifetime: keep partially
+      // written sectors in L2 (a partial-sector eviction costs a DRAM
+      // read-modify-write)
+      const uint32_t pos = wh[bk] + __popc(peers & lanemask_lt());
+      st_u32_keep(q.ent + pos, (((uint32_t)id & rmask) << q.bag_bits) | bag, pol_keep);
+    }
+    __syncwarp();
+    if (valid && (peers >> lane) == 1u) wh[bk] += __popc(peers);
+    __syncwarp();
+  };
   for (int64_t bw = wb0; bw < wb1; bw += kWarp) {
     const int nbg = (int)min64(kWarp, wb1 - bw);
     const int64_t oend = off[bw + nbg];
     const int64_t o = lane < nbg ? off[bw + lane] : oend;
+    // each lane finds its entry's bag by a shuffle search; ids of four rounds
+    // are loaded ahead
     const int64_t ostart = __shfl_sync(full, o, 0);
     for (int64_t pq = ostart; pq < oend; pq += 4 * kWarp) {
       int64_t idq[4];
@@ -387,20 +403,7 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
           const int64_t ok = __shfl_sync(full, o, k + step);
           if (ok <= p) k += step;
         }
-        const int64_t id = idq[u];
-        const bool valid = p < oend && id >= 0 && id < H;
-        const uint32_t bk = valid ? (uint32_t)(id >> s) : 0xffffffffu;
-        const unsigned peers = __match_any_sync(full, bk);
-        if (valid) {
-          // a bucket's entries land over the warp's lifetime: keep partially
-          // written sectors in L2 (a partial-sector eviction costs a DRAM
-          // read-modify-write)
-          const uint32_t pos = wh[bk] + __popc(peers & lanemask_lt());
-          st_u32_keep(q.ent + pos, (((uint32_t)id & rmask) << q.bag_bits) | (uint32_t)(bw + k), pol_keep);
-        }
-        __syncwarp();
-        if (valid && (peers >> lane) == 1u) wh[bk] += __popc(peers);
-        __syncwarp();
+        place(p, p < oend, idq[u], (uint32_t)(bw + k));
       }
     }
   }
@@ -1097,15 +1100,9 @@ __global__ void __launch_bounds__(kWW* kWarp) bkt_wsort_kernel(Params q, SegPara
     for (int d = lane; d < nbins; d += kWarp) sm.hist[d] = 0;
     cp_async_wait_all();
     __syncwarp();
-    // 1. digit histogram
-    for (int i0 = 0; i0 < n; i0 += kWarp) {
-      const int i = i0 + lane;
-      const bool v = i < n;
-      const uint32_t d = v ? (sm.in[i] >> bb) & dm : 0xffffffffu;
-      const unsigned peers = __match_any_sync(full, d);
-      if (v && (peers >> lane) == 1u) sm.hist[d] += (uint32_t)__popc(peers);
-      __syncwarp();
-    }
+    // 1. digit histogram (counts only: order does not matter here)
+    for (int i = lane; i < n; i += kWarp) atomicAdd(&sm.hist[(sm.in[i] >> bb) & dm], 1u);
+    __syncwarp();
     // 2. one scan: cursors (exclusive starts) and the touched rows in order
     const int per = (nbins + kWarp - 1) / kWarp;
     int cnt = 0, nz = 0;

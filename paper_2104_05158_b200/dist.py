@@ -51,7 +51,8 @@ class Comm:
 
     Byte accounting (the reference's byte contract, comms.py:366-540):
     ``sent[label][w]`` is what rank w sent to OTHER ranks through the
-    collectives labelled ``label`` ("lengths", "ids", "pooled", "grad");
+    collectives labelled ``label`` ("lengths", "ids", "pooled", "grad"),
+    ``recv[label][w]`` what it received from them;
     ``reduced[label][w]`` the payload bytes rank w contributed to an
     all-reduce (ring traffic is 2(W-1)/W of it, comms.py:433-439)."""
 
@@ -94,6 +95,7 @@ class NcclComm(Comm):
         sent = (sum(isp) - isp[self.ranks[0]]) * inp.element_size()
         self.bytes_sent += sent
         self._count("sent", label, self.ranks[0], sent)
+        self._count("recv", label, self.ranks[0], (sum(osp) - osp[self.ranks[0]]) * out.element_size())
         return self.dist.all_to_all_single(out, inp, osp, isp, group=self.group, async_op=async_op)
 
     def all_reduce_sum(self, tensors, label: str = "other") -> None:
@@ -125,6 +127,7 @@ class LocalComm(Comm):
                     if v != w:
                         self.bytes_sent += n * ins[w].element_size()
                         self._count("sent", label, w, n * ins[w].element_size())
+                        self._count("recv", label, v, n * ins[w].element_size())
 
     def all_reduce_sum(self, tensors, label: str = "other") -> None:
         for w, t in enumerate(tensors):

@@ -127,7 +127,7 @@ def multi_step_vs_local(rank, world, dev):
             local = nd.ShardedEmbedding(model, plan, lc, B, device=dev, dtype=torch.float32, optim="rowwise_adagrad",
                                         init=init, fwd_comm=fwd, bwd_comm=bwd, index_dtype=torch.int32)
             for k in range(3):
-                lb = _local_batches(batches[k], world)
+                lb = _local_batches(batches[k], world, torch.int32)
                 upk = torch.from_numpy(ups[k]).to(dev)
                 p_real = real.step([lb[rank]], lr=0.05, eps=1e-8,
                                    upstream_fn=lambda p: upk[rank * B:(rank + 1) * B])[0].clone()
@@ -141,10 +141,11 @@ def multi_step_vs_local(rank, world, dev):
                     if not torch.equal(mine[f"{s.table_id}#{s.index}"], w):
                         fails.append(f"{tag} step {k}: shard {s.table_id}#{s.index} differs")
             if transport == "nccl":
-                for label, per in lc.sent.items():
-                    got = real.comm.sent.get(label, [0] * world)[rank]
-                    if got != per[rank]:
-                        fails.append(f"{tag}: {label} bytes {got} != {per[rank]}")
+                for table in ("sent", "recv"):
+                    for label, per in getattr(lc, table).items():
+                        got = getattr(real.comm, table).get(label, [0] * world)[rank]
+                        if got != per[rank]:
+                            fails.append(f"{tag}: {table} {label} bytes {got} != {per[rank]}")
     if rank == 0 and not fails:
         print(f"dist_parity: world {world}: 3-step f32 (random upstream) and fp16/bf16-wire runs over NCCL and "
               "NVLink bitwise equal to the LocalComm engine; measured NCCL bytes equal per label", flush=True)

@@ -6,7 +6,8 @@ functions (oracle/_ref neosim.comms, comms.py:366-540):
 
 * pooled all-to-all (fwd)   == volume_forward_alltoall (TW/CW) + rw_reduce_scatter_fwd
                                (row-wise tables sharded over all W workers);
-* gradient all-to-all (bwd) == pooled_a2a_bwd + rw_gather_bwd (it mirrors the forward);
+* gradient all-to-all (bwd) == pooled_a2a_bwd + rw_gather_bwd, received by each shard owner
+                               (it mirrors the forward);
 * lengths phase             == volume_input_alltoall metadata_bytes (B x 8 per remote owner);
 * ids phase                 == volume_input_alltoall payload for TW/CW tables with integer
                                pooling (the reference's figure is an expectation; row-wise
@@ -89,7 +90,7 @@ def test_measured_bytes_equal_reference_volumes(pkg, ref, case):
     eng = dist.ShardedEmbedding(model, plan, comm, B, dtype=torch.float32, optim="sgd", fwd_comm=fwd,
                                 bwd_comm=bwd, index_dtype=torch.int32)
     batch = pkg.gen_synthetic_batch(model, W * B, seed=3 + case)
-    eng.step(_local_batches(batch, W), lr=0.05)
+    eng.step(_local_batches(batch, W, torch.int32), lr=0.05)
     torch.cuda.synchronize()
     # the reference's contract on the same plan / model
     rmodel = ref.ModelSpec(tables=tuple(ref.TableSpec(id=t.id, num_rows=t.num_rows, dim=t.dim,
@@ -109,8 +110,12 @@ def test_measured_bytes_equal_reference_volumes(pkg, ref, case):
         want_fwd = vf.per_worker_send_bytes[w] + (rs.per_worker_send_bytes[w] if rs else 0)
         want_bwd = vg["pooled_a2a_bwd"].per_worker_send_bytes[w] + (ga.per_worker_send_bytes[w] if ga else 0)
         assert comm.sent["pooled"][w] == want_fwd, (w, comm.sent["pooled"][w], want_fwd)
-        assert comm.sent["grad"][w] == want_bwd, (w, comm.sent["grad"][w], want_bwd)
+        # the backward mirrors the forward: the reference charges the shard owner, who RECEIVES
+        # the gradient rows of its shards (comms.py:409-418, rw_gather_bwd)
+        assert comm.recv["grad"][w] == want_bwd, (w, comm.recv["grad"][w], want_bwd)
         assert comm.sent["lengths"][w] == vi.metadata_bytes[w], (w, comm.sent["lengths"][w], vi.metadata_bytes[w])
+    for label in ("lengths", "ids", "pooled", "grad"):
+        assert sum(comm.sent[label]) == sum(comm.recv[label])
     # ids: TW/CW payload exactly (integer pooling); row-wise shares from the data
     L = np.asarray(batch.lengths)
     idx = np.asarray(batch.indices)

@@ -44,7 +44,10 @@ def test_reference_golden_streams(cache, golden):
 
 
 @pytest.mark.parametrize("ns,w,lfu,dist", [(4096, 32, 0, "uniform"), (4096, 32, 1, "zipf"), (977, 8, 1, "uniform"),
-                                           (50000, 4, 0, "zipf"), (1, 32, 0, "zipf"), (300, 1, 1, "uniform")])
+                                           (50000, 4, 0, "zipf"), (1, 32, 0, "zipf"), (300, 1, 1, "uniform"),
+                                           # more than one way per lane (the reference accepts any ways)
+                                           (1024, 48, 0, "uniform"), (512, 64, 1, "zipf"), (3, 100, 0, "zipf"),
+                                           (64, 128, 1, "uniform")])
 def test_large_traces_match_oracle(cache, ns, w, lfu, dist):
     rng = np.random.default_rng(ns + w)
     n = 400_000 if ns > 1 else 50_000
@@ -66,5 +69,5 @@ def test_error_contract(cache):
     with pytest.raises(cache.EmptyTrace):
         cache.simulate_trace(cache.CacheConfig(num_sets=4, ways=2), [])
     with pytest.raises(cache.InvalidValue):
-        cache.simulate_trace(cache.CacheConfig(num_sets=4, ways=33), [1])
+        cache.simulate_trace(cache.CacheConfig(num_sets=4, ways=129), [1])
     assert cache.simulate_trace(cache.CacheConfig(num_sets=2, ways=32), list(range(64)) * 2).hit_rate == 0.5
