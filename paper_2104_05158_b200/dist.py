@@ -148,6 +148,7 @@ class RankState:
     rank: int
     group: Optional[tbe.TableGroup] = None       # first non-empty local group (None: no shards)
     groups: list = field(default_factory=list)   # local TW/RW/CW shards, one TableGroup per overlap group
+    all_group: Optional[tbe.TableGroup] = None   # all local shards as one group (views)
     dp_group: Optional[tbe.TableGroup] = None    # replicated DP tables
     dp_dense: Optional[torch.Tensor] = None      # flat dense DP gradient buffer
     dp_dense_views: list = field(default_factory=list)
@@ -256,6 +257,19 @@ class ShardedEmbedding:
                     w.copy_(init(s.table, s.rows, s.cols).to(w.dtype))
             st.groups.append(grp)
         st.group = next((g for g in st.groups if g is not None), None)
+        # every local shard as ONE group (views of the overlap groups' tables):
+        # the NVLink transport moves the whole exchange at once, so its forward
+        # and fused backward run as single launches over all local shards
+        live = [g for g in st.groups if g is not None]
+        if len(live) > 1:
+            shards = lay.owned[r]
+            st.all_group = tbe.TableGroup([s.num_rows for s in shards], [s.dim for s in shards], dtype=self.dtype,
+                                          optim=self.optim, device=self.device,
+                                          weights=[w for g in live for w in g.weights],
+                                          moments=[m for g in live for m in g.moments],
+                                          table_ids=[f"{s.table_id}#{s.index}" for s in shards])
+        else:
+            st.all_group = st.group
         if lay.dp_tables:
             st.dp_group = tbe.TableGroup([lay.rows[t] for t in lay.dp_tables], [lay.dims[t] for t in lay.dp_tables],
                                          dtype=self.dtype, optim=self.optim, device=self.device,
@@ -313,14 +327,9 @@ class ShardedEmbedding:
         sc = st.sc
         ev.start("fwd")
         self._prepare_forward(st)
-        ef = _dtype_bytes(self.fwd_comm)
-        for g, grp in enumerate(st.groups):
-            if grp is None:
-                continue
-            k0, _ = self.gbounds[me][g]
-            ptrs = self.pool_dst + int(self.group_col[g]) * ef
-            grp.forward_scatter(sc["perm_ids"], sc["perm_off"][k0 * n:], n, ptrs, B, self.widths[me],
-                                self.fwd_comm)
+        if st.all_group is not None:
+            st.all_group.forward_scatter(sc["perm_ids"], sc["perm_off"], n, self.pool_dst, B, self.widths[me],
+                                         self.fwd_comm)
         self.hdl_pool.barrier(channel=0)  # every rank's rows have landed in every receive buffer
         ev.stop("fwd")
         pooled = self._assemble_sym(st)
@@ -330,13 +339,9 @@ class ShardedEmbedding:
         self.hdl_grad.barrier(channel=1)  # all upstream blocks have landed
         wd = self.widths[me]
         recv = self.sym_grad[:n * wd].view(n, wd) if wd else None
-        for gi, grp in enumerate(st.groups):
-            if grp is None:
-                continue
-            k0, k1 = self.gbounds[me][gi]
-            c0, c1 = int(self.group_col[gi]), int(self.group_col[gi + 1])
-            grp.backward(sc["perm_ids"], sc["perm_off"][k0 * n:], n, recv[:, c0:c1], mode="update",
-                         optim=self.optim, lr=lr, eps=eps, table_counts=sc["shard_counts"][k0:k1])
+        if st.all_group is not None:
+            st.all_group.backward(sc["perm_ids"], sc["perm_off"], n, recv, mode="update", optim=self.optim, lr=lr,
+                                  eps=eps, table_counts=sc["shard_counts"])
         self._backward_dp(st)
         ev.stop("bwd")
         return pooled

@@ -217,7 +217,7 @@ class TableGroup:
                 mode_code |= capi.NEO_BWD_FLAG_ALIGNED
                 if all(d == 32 * vec for d in self.dims):
                     mode_code |= capi.NEO_BWD_FLAG_FULL_ROWS
-        if self._bucketed(mode, batch, grad, stride, pooling, dense_grads):
+        if self._bucketed(mode, batch, grad, stride, pooling, dense_grads, table_counts):
             # hand-written bucketed sort + fused reduce/optimizer over the whole group
             mode_code |= capi.NEO_BWD_FLAG_DIM8
             n_b = n_idx if table_counts is None else int(sum(table_counts))
@@ -283,12 +283,19 @@ class TableGroup:
         return None
 
     def _bucketed(self, mode: str, batch: int, grad: torch.Tensor, stride: int, pooling: str,
-                  dense_grads=None) -> bool:
+                  dense_grads=None, table_counts=None) -> bool:
         """Mirror of the C side's bucketed-path condition (bkt_eligible):
         f32/f16 tables (f32 for DENSE), SUM, every D a multiple of 8 and
-        <= 256, 16-byte aligned rows and gradient."""
+        <= 256, 16-byte aligned rows and gradient.  Also routes to the
+        pipelined path groups whose tables would average more ids per row
+        bucket (a table has at most 2048 buckets) than one warp sorts in
+        shared memory: there every bucket would take the global-scratch sort."""
         if os.environ.get("NEO_BWD_VARIANT") in ("pipe", "stream"):
             return False
+        if table_counts is not None and os.environ.get("NEO_BWD_VARIANT") != "bucket":
+            for h, c in zip(self.rows, table_counts):
+                if h and c / min(2048, -(-h // 16)) > 1280:
+                    return False
         if pooling != "sum" or mode not in ("update", "dense") or self.max_dim > 256 or self.T == 0:
             return False
         if self.dtype not in (torch.float32, torch.float16) or (mode == "dense" and self.dtype != torch.float32):
@@ -321,7 +328,7 @@ class TableGroup:
         stride = grad.stride(0) if grad.dim() == 2 else self.total_dim
         if not self._streamed(batch, stride, pooling) or self.total_rows < 1:
             return False
-        if self._bucketed("update", batch, grad, stride, pooling):
+        if self._bucketed("update", batch, grad, stride, pooling, table_counts=table_counts):
             # the bucketed sort phase (count, scan, stable scatter, per-bucket
             # row sort, batch records) reads only the ids and writes only its
             # workspace, so it may run under the forward on a side stream

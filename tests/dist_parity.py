@@ -134,8 +134,19 @@ def multi_step_vs_local(rank, world, dev):
                 it = iter(range(world))
                 p_loc = local.step(lb, lr=0.05, eps=1e-8,
                                    upstream_fn=lambda p: upk[next(it) * B:][:B])
-                if not torch.equal(p_real, p_loc[rank]):
-                    fails.append(f"{tag} step {k}: pooled differs (max {(p_real - p_loc[rank]).abs().max().item()})")
+                # the data-parallel table (t4, the last 64 columns) is summed by NCCL's ring, whose
+                # order differs from the rank order LocalComm (and the reference, embedding.py:
+                # 195-205) uses once W > 2: its columns and replica agree to f32 rounding; every
+                # other column and shard must be bitwise equal
+                dpc = p_real.shape[1] - specs[4].dim
+                if not torch.equal(p_real[:, :dpc], p_loc[rank][:, :dpc]):
+                    fails.append(f"{tag} step {k}: pooled differs "
+                                 f"(max {(p_real[:, :dpc] - p_loc[rank][:, :dpc]).abs().max().item()})")
+                if not torch.allclose(p_real[:, dpc:], p_loc[rank][:, dpc:], rtol=1e-5, atol=1e-6):
+                    fails.append(f"{tag} step {k}: data-parallel pooled columns differ beyond f32 rounding")
+                if not torch.allclose(real.states[0].dp_group.weights[0], local.states[rank].dp_group.weights[0],
+                                      rtol=1e-5, atol=1e-6):
+                    fails.append(f"{tag} step {k}: data-parallel replica differs beyond f32 rounding")
                 mine = {f"{s.table_id}#{s.index}": w for s, w, _ in real.shard_tensors(0)}
                 for s, w, _ in local.shard_tensors(rank):
                     if not torch.equal(mine[f"{s.table_id}#{s.index}"], w):
@@ -148,7 +159,8 @@ def multi_step_vs_local(rank, world, dev):
                             fails.append(f"{tag}: {table} {label} bytes {got} != {per[rank]}")
     if rank == 0 and not fails:
         print(f"dist_parity: world {world}: 3-step f32 (random upstream) and fp16/bf16-wire runs over NCCL and "
-              "NVLink bitwise equal to the LocalComm engine; measured NCCL bytes equal per label", flush=True)
+              "NVLink bitwise equal to the LocalComm engine (data-parallel table: within f32 rounding of the "
+              "ring all-reduce); measured NCCL bytes equal per label", flush=True)
     return fails
 
 
