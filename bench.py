@@ -111,7 +111,7 @@ class Clocks:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(index), "-lms", "100"],
+                 "-i", str(index), "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
@@ -431,6 +431,10 @@ def run_b200(a, rank, world):
     overlap = a.overlap_sort >= 0 and counts is not None
     if overlap:
         tbe.set_forward_residency(a.overlap_sort)
+        # the step runs on a high-priority stream: the block scheduler then
+        # places the forward's CTAs first and the side-stream sort phase fills
+        # the SM resources the capped forward leaves free
+        torch.cuda.set_stream(torch.cuda.Stream(device=dev, priority=-1))
 
     def step(i):
         ix = batches[i % 2]
@@ -440,13 +444,15 @@ def run_b200(a, rank, world):
         grp.backward(ix, offsets, B, upstream, mode="update", optim="rowwise_adagrad", lr=LR, eps=EPS,
                      table_counts=counts)
 
+    # nvidia-smi starts before the warm-up: its start-up (NVML init) can stall
+    # driver calls for tens of ms, which must not land inside the timed steps
+    clocks = Clocks(dev.index)
     for i in range(a.warmup):
         step(i)
     launches_per_step = count_launches(lambda: step(0))
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    clocks = Clocks(dev.index)
     time.sleep(0.3)
     torch.cuda.synchronize()
     timers = {}
@@ -696,34 +702,35 @@ def run_sharded(a, rank, world, dev):
     def step(i, timers=None):
         return eng.step([(lengths, ids[i % 2], L_dev)], lr=LR, eps=EPS, timers=timers)
 
+    clocks = Clocks(dev.index) if rank == 0 else None  # before the warm-up (see run_b200)
     for i in range(a.warmup):
         step(i)
     launches_per_step = count_launches(lambda: step(0))
     torch.cuda.synchronize()
     tdist.barrier()
-    clocks = Clocks(dev.index) if rank == 0 else None
     time.sleep(0.3)
     timers = {}
     torch.cuda.synchronize()
     tdist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+    evs[0].record()
     for i in range(a.steps):
         step(i, timers)
-    e1.record()
+        evs[i + 1].record()
     torch.cuda.synchronize()
     tdist.barrier()
     clk = clocks.stop() if clocks else None
-    ms_local = e0.elapsed_time(e1) / a.steps
+    ms_local = evs[0].elapsed_time(evs[-1]) / a.steps
+    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(a.steps)]
     ph = {k: float(np.mean([x.elapsed_time(y) for x, y in v])) for k, v in timers.items()}
     n = B * world
     fb_local = local_fwd_bytes(eng, wl, n, B)
     fwd_gbs_local = fb_local / (ph.get("fwd", 1.0) * 1e-3) / 1e9
     t = torch.tensor([ms_local, ph.get("fwd", 0.0), ph.get("bwd", 0.0), ph.get("a2a_fwd", 0.0),
-                      ph.get("a2a_bwd", 0.0), fb_local], dtype=torch.float64, device=dev)
+                      ph.get("a2a_bwd", 0.0), fb_local, ph.get("inputs", 0.0), ph.get("dp", 0.0)],
+                     dtype=torch.float64, device=dev)
     tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-    ms, fwd_ms, bwd_ms, a2f_ms, a2b_ms, fb_max = t.tolist()
+    ms, fwd_ms, bwd_ms, a2f_ms, a2b_ms, fb_max, in_ms, dp_ms = t.tolist()
     tmin = torch.tensor([fwd_gbs_local], dtype=torch.float64, device=dev)
     tdist.all_reduce(tmin, op=tdist.ReduceOp.MIN)
     busbw = alltoall_busbw(eng, dev, world)
@@ -752,7 +759,9 @@ def run_sharded(a, rank, world, dev):
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": fwd_gbs / peak, "traffic": None,
                      "algorithmic_bytes": fb_max, "ms": fwd_ms, "min_rank_gbs": float(tmin.item())},
         "phases_ms": {"fwd_incl_overlapped_a2a": fwd_ms, "a2a_fwd_tail": a2f_ms,
-                      "bwd_incl_overlapped_a2a": bwd_ms, "overlap_groups": eng.G, "transport": a.transport},
+                      "bwd_incl_overlapped_a2a": bwd_ms, "input_exchange": in_ms, "dp_allreduce_update": dp_ms,
+                      "overlap_groups": eng.G, "transport": a.transport,
+                      "rank0_step_ms": [round(x, 3) for x in per_step]},
         "alltoall": {"send_bytes_per_gpu": send, "busbw_gbs": busbw["busbw_gbs"], "ms": busbw["ms"],
                      "peak_gbs": 900.0, "frac_of_nominal": busbw["busbw_gbs"] / 900.0,
                      "note": "pooled all-to-all payload of one step (per-GPU send bytes excluding self, "

@@ -31,6 +31,7 @@
  *                              (fp16 fwd / bf16 bwd payloads)
  *   neo_lengths_to_offsets     model.py:365-370 lengths_to_offsets
  *   neo_bucketize_rowwise      comms.py:107-141 bucketize_rowwise
+ *   neo_bucketize_rowwise_multi comms.py:107-141 (every row-wise table of a batch in one call)
  *   neo_permute_blocks         comms.py:222-257 permute_WTB_to_TWB /
  *                              permute_TWB_to_WTB (and to_wtb, comms.py:197)
  *   neo_copy_pieces            comms.py:692-711 pooled assembly (TW copy,
@@ -228,6 +229,20 @@ int neo_bucketize_rowwise(int64_t n, const int64_t* offsets, const void* indices
                           int64_t* out_lengths, int64_t* out_offsets, void* out_indices,
                           int32_t table, neo_error* err,
                           void* workspace, size_t workspace_bytes, void* stream);
+
+/* Row-wise bucketisation of many tables in one call (the sharded step's
+ * sender side, comms.py:107-141 applied per row-wise table): tables[r]
+ * (device, num_rw) names table r's bags in the full batch (offsets over
+ * T*batch bags, device); shard_starts (device, num_rw x (kmax+1)) holds table
+ * r's shard_counts[r] + 1 boundaries.  out_lengths (num_rw, kmax, batch),
+ * out_offsets its exclusive scan (num_rw*kmax*batch + 1), out_indices the ids
+ * grouped by (table, shard, bag), rebased to the shard.  Ids outside their
+ * table are skipped (validate them first with neo_check_indices).
+ * Workspace: neo_bucketize_workspace_bytes(num_rw * batch, kmax). */
+int neo_bucketize_rowwise_multi(int32_t num_rw, int64_t batch, const int32_t* tables, const int64_t* offsets,
+                                const void* indices, int32_t index_dtype, int32_t kmax, const int64_t* shard_starts,
+                                const int32_t* shard_counts, int64_t* out_lengths, int64_t* out_offsets,
+                                void* out_indices, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- block permute (comms.py:222-264) ----------------------------------
  * lengths: outer*inner*B entries whose (o, i) block of B lengths covers the

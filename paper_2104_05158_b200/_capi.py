@@ -85,6 +85,7 @@ SIGNATURES = {
         C.c_int,
         [I64, P, P, I32, I32, C.POINTER(C.c_int64), P, P, P, I32, P, P, SZ, P],
     ),
+    "neo_bucketize_rowwise_multi": (C.c_int, [I32, I64, P, P, P, I32, I32, P, P, P, P, P, P, SZ, P]),
     "neo_permute_workspace_bytes": (SZ, [I32, I32]),
     "neo_permute_blocks": (C.c_int, [I32, I32, I64, P, P, I32, P, P, P, SZ, P]),
     "neo_copy_pieces": (C.c_int, [I64, P, I32, I32, I32, P]),

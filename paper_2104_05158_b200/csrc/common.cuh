@@ -16,6 +16,7 @@ namespace neo {
 constexpr int kWarp = 32;
 
 __host__ __device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 // thread-local message for neo_last_error()
 void set_error(const std::string& msg);

@@ -95,6 +95,66 @@ bucketize_kernel(int64_t n, const int64_t* __restrict__ offsets, const Idx* __re
     for (int s = lane; s < k; s += kWarp) out_lengths[(int64_t)s * n + b] = cnt[s];
 }
 
+// Many row-wise tables in one launch (the sharded step's sender side): warp
+// per (row-wise table r, bag b); table r is tables[r] of the full batch
+// (global offsets over T*B bags), its shard boundaries starts[r][0..k_r].
+// Output blocks are (r, shard, bag) ordered with kmax shard slots per table
+// (unused slots stay empty), so one scan gives every block's offsets.
+template <typename Idx, bool kScatter>
+__global__ void __launch_bounds__(256)
+bucketize_multi_kernel(int32_t R, int64_t B, const int32_t* __restrict__ tables,
+                       const int64_t* __restrict__ offsets, const Idx* __restrict__ indices, int32_t kmax,
+                       const int64_t* __restrict__ starts, const int32_t* __restrict__ kk,
+                       int64_t* __restrict__ out_lengths, const int64_t* __restrict__ out_offsets,
+                       Idx* __restrict__ out_indices) {
+  __shared__ int32_t s_cnt[8][kMaxShards];
+  __shared__ int64_t s_st[8][kMaxShards + 1];
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int64_t g = (int64_t)blockIdx.x * 8 + warp;
+  if (g >= (int64_t)R * B) return;
+  const int r = (int)(g / B);
+  const int64_t b = g - (int64_t)r * B;
+  const int k = kk[r];
+  int32_t* cnt = s_cnt[warp];
+  int64_t* st = s_st[warp];
+  for (int i = lane; i < kMaxShards; i += kWarp) cnt[i] = 0;
+  for (int i = lane; i <= k; i += kWarp) st[i] = starts[(int64_t)r * (kmax + 1) + i];
+  __syncwarp();
+  const int64_t gb = (int64_t)tables[r] * B + b;
+  const int64_t start = offsets[gb], end = offsets[gb + 1];
+  const int64_t H = st[k];
+  const int64_t blk0 = (int64_t)r * kmax;
+  for (int64_t base = start; base < end; base += kWarp) {
+    const int64_t p = base + lane;
+    int sh = -1;
+    int64_t x = 0;
+    if (p < end) {
+      x = (int64_t)indices[p];
+      if (x >= 0 && x < H) {  // ids outside the table were reported by neo_check_indices
+        int lo = 0, hi = k - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) / 2;
+          if (x < st[mid + 1]) hi = mid;
+          else lo = mid + 1;
+        }
+        sh = lo;
+      }
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, sh);
+    const int leader = __ffs(peers) - 1;
+    if (kScatter && sh >= 0) {
+      const unsigned lt = peers & ((1u << lane) - 1u);
+      const int64_t pos = out_offsets[(blk0 + sh) * B + b] + cnt[sh] + __popc(lt);
+      out_indices[pos] = (Idx)(x - st[sh]);
+    }
+    __syncwarp();
+    if (sh >= 0 && lane == leader) cnt[sh] += __popc(peers);
+    __syncwarp();
+  }
+  if (!kScatter)
+    for (int i = lane; i < kmax; i += kWarp) out_lengths[(blk0 + i) * B + b] = cnt[i];
+}
+
 // ---------------------------------------------------------------------------
 // block permute (comms.py:222-257)
 
@@ -283,6 +343,42 @@ int neo_lengths_to_offsets(int64_t n, const int64_t* lengths, int64_t* offsets, 
   if (workspace_bytes < inclusive_scan_temp(n))
     return fail(NEO_E_ARG, "lengths_to_offsets: workspace too small");
   return scan_lengths(n, lengths, offsets, workspace, workspace_bytes, as_stream(stream));
+}
+
+int neo_bucketize_rowwise_multi(int32_t num_rw, int64_t batch, const int32_t* tables, const int64_t* offsets,
+                                const void* indices, int32_t index_dtype, int32_t kmax, const int64_t* shard_starts,
+                                const int32_t* shard_counts, int64_t* out_lengths, int64_t* out_offsets,
+                                void* out_indices, void* workspace, size_t workspace_bytes, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (num_rw < 0 || batch < 0 || kmax < 1) return fail(NEO_E_ARG, "bucketize_multi: bad sizes");
+  if (kmax > kMaxShards) return fail(NEO_E_ARG, "bucketize_multi: at most 64 row shards");
+  if (index_dtype != NEO_I32 && index_dtype != NEO_I64)
+    return fail(NEO_E_ARG, "bucketize_multi: index dtype must be I32 or I64");
+  const int64_t n = (int64_t)num_rw * batch;
+  if (workspace_bytes < inclusive_scan_temp((int64_t)kmax * n))
+    return fail(NEO_E_ARG, "bucketize_multi: workspace too small");
+  if (n == 0) {
+    if (cudaMemsetAsync(out_offsets, 0, sizeof(int64_t), s) != cudaSuccess)
+      return fail(NEO_E_CUDA, "bucketize_multi: memset failed");
+    return NEO_OK;
+  }
+  if (!tables || !offsets || !shard_starts || !shard_counts || !out_lengths || !out_offsets)
+    return fail(NEO_E_ARG, "bucketize_multi: null pointer");
+  const unsigned grid = (unsigned)((n + 7) / 8);
+#define NEO_BKM(IDX, SC, OUT)                                                                              \
+  bucketize_multi_kernel<IDX, SC><<<grid, 256, 0, s>>>(num_rw, batch, tables, offsets, (const IDX*)indices, \
+                                                       kmax, shard_starts, shard_counts, out_lengths,      \
+                                                       SC ? out_offsets : nullptr, (IDX*)OUT)
+  if (index_dtype == NEO_I32) NEO_BKM(int32_t, false, nullptr);
+  else NEO_BKM(int64_t, false, nullptr);
+  int rc = check_launch("bucketize_multi(count)");
+  if (rc) return rc;
+  rc = scan_lengths((int64_t)kmax * n, out_lengths, out_offsets, workspace, workspace_bytes, s);
+  if (rc) return rc;
+  if (index_dtype == NEO_I32) NEO_BKM(int32_t, true, out_indices);
+  else NEO_BKM(int64_t, true, out_indices);
+#undef NEO_BKM
+  return check_launch("bucketize_multi(scatter)");
 }
 
 size_t neo_bucketize_workspace_bytes(int64_t n, int32_t k) {

@@ -341,16 +341,23 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
   const int64_t* off = q.offsets + (int64_t)t * q.B;
   const int64_t p0 = off[wb0], p1 = off[wb1];
   uint32_t* wh = hist + warp * nb;
-  for (int64_t pb = p0; pb < p1; pb += 4 * kWarp) {  // four independent loads in flight per lane
-    int64_t id[4];
+  // count pass: the next group's ids are in flight while this group's are counted
+  constexpr int kCU = 8;
+  auto ld_id = [&](int64_t p) -> int64_t { return p < p1 ? (int64_t)indices[p] : -1; };
+  {
+    int64_t cur[kCU];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t p = pb + u * kWarp + lane;
-      id[u] = p < p1 ? (int64_t)indices[p] : -1;
+    for (int u = 0; u < kCU; ++u) cur[u] = ld_id(p0 + u * kWarp + lane);
+    for (int64_t pb = p0; pb < p1; pb += kCU * kWarp) {
+      int64_t nxt[kCU];
+#pragma unroll
+      for (int u = 0; u < kCU; ++u) nxt[u] = ld_id(pb + (kCU + u) * kWarp + lane);
+#pragma unroll
+      for (int u = 0; u < kCU; ++u)
+        if (cur[u] >= 0 && cur[u] < H) atomicAdd(&wh[(int)(cur[u] >> s)], 1u);
+#pragma unroll
+      for (int u = 0; u < kCU; ++u) cur[u] = nxt[u];
     }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (id[u] >= 0 && id[u] < H) atomicAdd(&wh[(int)(id[u] >> s)], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x) {
@@ -362,50 +369,77 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
     }
   }
   __syncthreads();
-  // place in buffer order, 32 bags per window
-  auto place = [&](int64_t p, bool in, int64_t id, uint32_t bag) {
-    const bool valid = in && id >= 0 && id < H;
-    const uint32_t bk = valid ? (uint32_t)(id >> s) : 0xffffffffu;
-    const unsigned peers = __match_any_sync(full, bk);
-    if (valid) {
-      // a bucket's entries land over the warp's lifetime: keep partially
-      // written sectors in L2 (a partial-sector eviction costs a DRAM
-      // read-modify-write)
-      const uint32_t pos = wh[bk] + __popc(peers & lanemask_lt());
-      st_u32_keep(q.ent + pos, (((uint32_t)id & rmask) << q.bag_bits) | bag, pol_keep);
-    }
-    __syncwarp();
-    if (valid && (peers >> lane) == 1u) wh[bk] += __popc(peers);
-    __syncwarp();
-  };
-  for (int64_t bw = wb0; bw < wb1; bw += kWarp) {
-    const int nbg = (int)min64(kWarp, wb1 - bw);
-    const int64_t oend = off[bw + nbg];
-    const int64_t o = lane < nbg ? off[bw + lane] : oend;
-    // each lane finds its entry's bag by a shuffle search; ids of four rounds
-    // are loaded ahead
-    const int64_t ostart = __shfl_sync(full, o, 0);
-    for (int64_t pq = ostart; pq < oend; pq += 4 * kWarp) {
-      int64_t idq[4];
+  // place pass, in buffer order.  Rounds of 32 consecutive entries; a window
+  // of 32 bags (offsets relative to the window start, one per lane) resolves
+  // each entry's bag; the next window's offsets and the next group's ids are
+  // loaded ahead.  Within a round, equal buckets are ranked by lane
+  // (match_any) and the group's leader reserves the slots with one shared
+  // atomic, so rounds chain only through the atomics.
+  const unsigned lt = lanemask_lt();
+  auto win_off = [&](int64_t bw) -> int64_t { return bw + lane < wb1 ? off[bw + lane] : p1; };
+  int64_t bw = wb0;
+  int64_t obase = off[wb0];
+  int64_t o64 = win_off(bw);
+  int64_t onext = win_off(bw + kWarp);
+  uint32_t orel = (uint32_t)(o64 - obase);
+  int64_t wend = bw + kWarp < wb1 ? __shfl_sync(full, onext, 0) : p1;
+  constexpr int kPU = 4;
+  int64_t cur[kPU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t p = pq + u * kWarp + lane;
-        idq[u] = p < oend ? (int64_t)indices[p] : -1;
-      }
+  for (int u = 0; u < kPU; ++u) cur[u] = ld_id(p0 + u * kWarp + lane);
+  for (int64_t pq = p0; pq < p1; pq += kPU * kWarp) {
+    int64_t nxt[kPU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int64_t pb = pq + u * kWarp;
-        if (pb >= oend) break;  // warp-uniform
-        const int64_t p = pb + lane;
-        int k = 0;  // last bag of the window starting at or before p
+    for (int u = 0; u < kPU; ++u) nxt[u] = ld_id(pq + (kPU + u) * kWarp + lane);
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int64_t ok = __shfl_sync(full, o, k + step);
-          if (ok <= p) k += step;
+    for (int u = 0; u < kPU; ++u) {
+      const int64_t pb = pq + u * kWarp;
+      if (pb >= p1) break;  // warp-uniform
+      const int64_t p = pb + lane;
+      const int64_t id = cur[u];
+      int64_t lo = pb;  // first position of the round not yet placed
+      for (;;) {
+        const int64_t lim = min64(min64(pb + kWarp, p1), wend);
+        const bool in = p >= lo && p < lim;
+        // bag: the last window lane whose start is <= p
+        const uint32_t prel = (uint32_t)(min64(max64(p, lo), lim - 1) - obase);
+        const uint32_t ja = 31 - __clz(__ballot_sync(full, orel <= (uint32_t)(lo - obase)));
+        const uint32_t jb = 31 - __clz(__ballot_sync(full, orel <= (uint32_t)(lim - 1 - obase)));
+        uint32_t k = ja;
+        if (ja != jb) {  // a bag starts inside the round: per-lane search
+          k = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t ok = __shfl_sync(full, orel, k + step);
+            if (ok <= prel) k += step;
+          }
         }
-        place(p, p < oend, idq[u], (uint32_t)(bw + k));
+        const bool valid = in && id >= 0 && id < H;
+        const uint32_t bk = valid ? (uint32_t)(id >> s) : 0xffffffffu;
+        const unsigned peers = __match_any_sync(full, bk);
+        const int leader = __ffs(peers) - 1;
+        uint32_t at = 0;
+        if (valid && lane == leader) at = atomicAdd(&wh[bk], (uint32_t)__popc(peers));
+        at = __shfl_sync(full, at, leader);
+        // a bucket's entries land over the warp's lifetime: keep partially
+        // written sectors in L2 (a partial-sector eviction costs a DRAM
+        // read-modify-write)
+        if (valid)
+          st_u32_keep(q.ent + at + __popc(peers & lt), (((uint32_t)id & rmask) << q.bag_bits) | (uint32_t)(bw + k),
+                      pol_keep);
+        if (lim == min64(pb + kWarp, p1)) break;
+        // the round continues past the window: the next window
+        lo = lim;
+        bw += kWarp;
+        obase = wend;
+        o64 = onext;
+        onext = win_off(bw + kWarp);
+        orel = (uint32_t)(o64 - obase);
+        wend = bw + kWarp < wb1 ? __shfl_sync(full, onext, 0) : p1;
       }
     }
+#pragma unroll
+    for (int u = 0; u < kPU; ++u) cur[u] = nxt[u];
   }
 }
 

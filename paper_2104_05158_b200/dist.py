@@ -220,6 +220,23 @@ class ShardedEmbedding:
         for t, bounds in lay.rw_bounds.items():
             for s in (s for v in range(self.W) for s in lay.owned[v] if s.table == t):
                 self.rw_slot[(t, s.index)] = bounds.index(s.rows)
+        # every row-wise table is bucketised in ONE launch per step
+        # (neo_bucketize_rowwise_multi): table r's shard boundaries padded to
+        # kmax slots; send blocks located by (table, shard slot) -> flat block
+        self.rw_tables = sorted(lay.rw_bounds)
+        self.rw_kmax = max((len(b) for b in lay.rw_bounds.values()), default=1)
+        self.rw_starts = np.zeros((len(self.rw_tables), self.rw_kmax + 1), dtype=np.int64)
+        self.rw_k = np.zeros(len(self.rw_tables), dtype=np.int32)
+        for r, t in enumerate(self.rw_tables):
+            b = lay.rw_bounds[t]
+            self.rw_starts[r, :len(b)] = [x[0] for x in b]
+            self.rw_starts[r, len(b):] = b[-1][1]
+            self.rw_k[r] = len(b)
+        rpos = {t: r for r, t in enumerate(self.rw_tables)}
+        self.blk_table = np.array([s.table for _, s in self.send_blocks], dtype=np.int64)
+        self.blk_rw = np.array([s.kind == "row_wise" for _, s in self.send_blocks], dtype=bool)
+        self.blk_flat = np.array([rpos[s.table] * self.rw_kmax + self.rw_slot[(s.table, s.index)]
+                                  if s.kind == "row_wise" else 0 for _, s in self.send_blocks], dtype=np.int64)
         self.dp_cols = {}
         c = 0
         for t in lay.dp_tables:
@@ -459,17 +476,21 @@ class ShardedEmbedding:
         for local rank slot i.  Returns the pooled (B, sum D) outputs per
         local rank (model table order).  upstream_fn(pooled) -> gradient
         (default: ones, the reference's sum-of-outputs loss).  timers: dict
-        receiving CUDA event pairs for "fwd", "a2a_fwd", "a2a_bwd", "bwd"."""
+        receiving CUDA event pairs for "inputs", "fwd", "a2a_fwd", "a2a_bwd", "bwd", "dp"."""
         W, B = self.W, self.B
         S = self.states
         ev = _Timers(timers)
+        ev.start("inputs")
         self._exchange_inputs(batches)
+        ev.stop("inputs")
         if self.transport == "nvlink":
             pooled = [self._step_nvlink(S[0], lr, eps, upstream_fn, ev)]
             if self.lay.dp_tables:
+                ev.start("dp")
                 self.comm.all_reduce_sum([st.dp_dense for st in S], label="dp")
                 for st in S:
                     self._dp_update(st, lr, eps)
+                ev.stop("dp")
             return pooled
         ev.start("fwd")
         for st in S:
@@ -510,9 +531,11 @@ class ShardedEmbedding:
             self._backward_dp(st)
         ev.stop("bwd")
         if self.lay.dp_tables:
+            ev.start("dp")
             self.comm.all_reduce_sum([st.dp_dense for st in S], label="dp")
             for st in S:
                 self._dp_update(st, lr, eps)
+            ev.stop("dp")
         return pooled
 
     def redistribute(self, batches: Sequence) -> list:
@@ -574,53 +597,54 @@ class ShardedEmbedding:
             st.cache["rows_dev"] = torch.tensor([t.num_rows for t in self.model.tables], dtype=torch.int64,
                                                 device=dev)
         err.reset()
+        g_off = tbe.lengths_to_offsets(L_dev)
         if ids.numel():
-            tbe.check_indices(st.cache["rows_dev"], tbe.lengths_to_offsets(L_dev), ids, B, err)
+            tbe.check_indices(st.cache["rows_dev"], g_off, ids, B, err)
         es = ids.element_size()
-        rw = {}
-        for t, bounds in lay.rw_bounds.items():  # bucketise this rank's block per row-wise table
-            starts = [b[0] for b in bounds] + [bounds[-1][1]]
-            sub = ids[int(tab_off[t]):int(tab_off[t + 1])]
-            if sub.numel() == 0:
-                sub = torch.zeros(1, dtype=ids.dtype, device=dev)
-            rw[t] = tbe.bucketize_rowwise(tbe.lengths_to_offsets(L_dev[t * B:(t + 1) * B]), sub, starts)
-        sc["rw"] = rw
         nb = len(self.send_blocks)
         nS = len(lay.owned[st.rank])
         sc["recv_len"] = self._buf(st, "recv_len", W * nS * B, torch.int64)
         sc["send_len"] = self._buf(st, "send_len", nb * B, torch.int64)
+        R, kmax = len(self.rw_tables), self.rw_kmax
+        if R:  # bucketise this rank's block of every row-wise table, one launch
+            meta = st.cache.get("rw_meta")
+            if meta is None:
+                meta = (torch.tensor(self.rw_tables, dtype=torch.int32, device=dev),
+                        torch.from_numpy(self.rw_starts.reshape(-1)).to(dev),
+                        torch.from_numpy(self.rw_k).to(dev))
+                st.cache["rw_meta"] = meta
+            rw_len = self._buf(st, "rw_len", R * kmax * B, torch.int64)[:R * kmax * B]
+            rw_off = self._buf(st, "rw_off", R * kmax * B + 1, torch.int64)[:R * kmax * B + 1]
+            n_rw = int(sum(cnt[t] for t in self.rw_tables))
+            rw_idx = self._buf(st, "rw_idx", max(n_rw, 1), ids.dtype)
+            ws = tbe.WORKSPACE.get("bucketize", tbe.capi.lib().neo_bucketize_workspace_bytes(R * B, kmax), dev)
+            tbe.capi.check(tbe.capi.lib().neo_bucketize_rowwise_multi(
+                R, B, meta[0].data_ptr(), g_off.data_ptr(), ids.data_ptr(), tbe.INDEX_CODE[ids.dtype], kmax,
+                meta[1].data_ptr(), meta[2].data_ptr(), rw_len.data_ptr(), rw_off.data_ptr(), rw_idx.data_ptr(),
+                ws.data_ptr(), ws.numel(), tbe._stream()), "neo_bucketize_rowwise_multi")
         if not nb:
             sc["send_counts"] = torch.zeros(W, dtype=torch.int64, device=dev)
             sc["blk"] = None
             return
-        len_ptr = np.empty(nb, dtype=np.int64)
-        ptr = np.empty(nb, dtype=np.int64)
-        cnt_h = np.empty(nb, dtype=np.int64)
-        rw_pos, rw_ref = [], []
-        base_L = L_dev.data_ptr()
-        for i, (v, s) in enumerate(self.send_blocks):
-            if s.kind == "row_wise":
-                j = self.rw_slot[(s.table, s.index)]
-                o_len, o_off, o_idx = rw[s.table]
-                len_ptr[i] = o_len[j].data_ptr()
-                ptr[i] = o_idx.data_ptr()
-                cnt_h[i] = 0
-                rw_pos.append(i)
-                rw_ref.append((s.table, j))
-            else:
-                len_ptr[i] = base_L + s.table * B * 8
-                ptr[i] = ids.data_ptr() + int(tab_off[s.table]) * es
-                cnt_h[i] = int(cnt[s.table])
+        rwm, tabs = self.blk_rw, self.blk_table
+        len_ptr = np.where(rwm, (rw_len.data_ptr() if R else 0) + self.blk_flat * B * 8, L_dev.data_ptr() + tabs * B * 8)
+        ptr = np.where(rwm, rw_idx.data_ptr() if R else 0, ids.data_ptr() + tab_off[tabs] * es)
+        cnt_h = np.where(rwm, 0, cnt[tabs])
         meta = torch.from_numpy(np.stack([len_ptr, np.full(nb, B, np.int64), np.arange(nb, dtype=np.int64) * B,
-                                          ptr, cnt_h])).to(dev, non_blocking=False)
+                                          ptr, cnt_h]).astype(np.int64)).to(dev, non_blocking=False)
         tbe.gather_blocks_dev(meta[0], meta[1], meta[2], sc["send_len"])
         ptr_dev, cnt_dev = meta[3].clone(), meta[4].clone()
-        if rw_pos:  # row-wise block sizes / starts live on the device
-            pos = torch.tensor(rw_pos, dtype=torch.int64, device=dev)
-            lo = torch.stack([rw[t][1][j * B] for t, j in rw_ref])
-            hi = torch.stack([rw[t][1][(j + 1) * B] for t, j in rw_ref])
-            ptr_dev.index_add_(0, pos, lo * es)
-            cnt_dev.index_copy_(0, pos, hi - lo)
+        if R and rwm.any():  # row-wise block sizes / starts live on the device
+            sel = st.cache.get("rw_sel")
+            if sel is None:
+                pos_h = np.nonzero(rwm)[0]
+                sel = (torch.from_numpy(pos_h).to(dev), torch.from_numpy(self.blk_flat[pos_h] * B).to(dev),
+                       torch.from_numpy((self.blk_flat[pos_h] + 1) * B).to(dev))
+                st.cache["rw_sel"] = sel
+            lo = rw_off.index_select(0, sel[1])
+            hi = rw_off.index_select(0, sel[2])
+            ptr_dev.index_add_(0, sel[0], lo * es)
+            cnt_dev.index_copy_(0, sel[0], hi - lo)
         dst_dev = torch.cumsum(cnt_dev, 0) - cnt_dev
         dest = self._dest_index(st)
         sc["send_counts"] = torch.zeros(W, dtype=torch.int64, device=dev).index_add_(0, dest, cnt_dev)

@@ -95,6 +95,18 @@ def _u64_ptrs(tensors, device) -> torch.Tensor:
                         device=device)
 
 
+def _bucket_bits(h: int, n: int, target: int = 1024) -> int:
+    """Row bits per bucket bkt_setup_kernel picks for a table of h rows and n
+    ids (tbe_bucket.cu: <= 2048 buckets, about `target` ids per bucket)."""
+    s = 4
+    while -(-h // (1 << s)) > 2048:
+        s += 1
+    hb = max(0, (h - 1).bit_length()) if h > 1 else 0
+    while s < hb and n * (1 << s) < target * h:
+        s += 1
+    return s
+
+
 class TableGroup:
     """T embedding tables sharing one TBE launch.
 
@@ -287,15 +299,19 @@ class TableGroup:
         """Mirror of the C side's bucketed-path condition (bkt_eligible):
         f32/f16 tables (f32 for DENSE), SUM, every D a multiple of 8 and
         <= 256, 16-byte aligned rows and gradient.  Also routes to the
-        pipelined path groups whose tables would average more ids per row
-        bucket (a table has at most 2048 buckets) than one warp sorts in
-        shared memory: there every bucket would take the global-scratch sort."""
+        pipelined path groups with a table whose row buckets would span more
+        than 2^9 rows or average more than 1280 ids (bkt_setup_kernel's
+        rule, at most 2048 buckets per table): those buckets miss the
+        warp-per-bucket sort and take the CTA sort, which is slower than the
+        pipelined walk (measured on c3 / c5 at 4 GPUs)."""
         if os.environ.get("NEO_BWD_VARIANT") in ("pipe", "stream"):
             return False
         if table_counts is not None and os.environ.get("NEO_BWD_VARIANT") != "bucket":
             for h, c in zip(self.rows, table_counts):
-                if h and c / min(2048, -(-h // 16)) > 1280:
-                    return False
+                if h and c:
+                    sb = _bucket_bits(h, c)
+                    if sb > 9 or c * (1 << sb) > 1280 * h:  # CTA-sorted buckets (see below)
+                        return False
         if pooling != "sum" or mode not in ("update", "dense") or self.max_dim > 256 or self.T == 0:
             return False
         if self.dtype not in (torch.float32, torch.float16) or (mode == "dense" and self.dtype != torch.float32):

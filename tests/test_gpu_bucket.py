@@ -108,8 +108,11 @@ def test_bucket_matches_oracle_and_is_deterministic(tbe, case):
     _check_oracle(grp, init_w, init_m, lengths, idx, up.double().cpu().numpy(), rows, dims, optim, wdt, f"case {case}")
 
 
-def test_bucket_int64_ids_and_table_counts(tbe):
-    """int64 ids; the call with host table counts takes the same path."""
+def test_bucket_int64_ids_and_table_counts(tbe, monkeypatch):
+    """int64 ids; the call with host table counts takes the same path (forced:
+    with counts, tables whose buckets span > 2^9 rows route to the pipelined
+    walk by default)."""
+    monkeypatch.setenv("NEO_BWD_VARIANT", "bucket")
     rows, dims, B = [70000, 90000], [128, 64], 4096
     rng = np.random.default_rng(11)
     lengths = rng.integers(0, 30, size=(2, B))
