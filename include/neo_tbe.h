@@ -36,6 +36,7 @@
  *                              permute_TWB_to_WTB (and to_wtb, comms.py:197)
  *   neo_copy_pieces            comms.py:692-711 pooled assembly (TW copy,
  *                              CW column placement, RW partial sum)
+ *   neo_copy_chunks            comms.py:692-711 (the same, narrow blocks lane-parallel)
  *   neo_gather_blocks          comms.py:292-353 alltoall_redistribute send
  *                              packing; comms.py:164-172 replicate_columnwise
  */
@@ -270,6 +271,21 @@ typedef struct neo_piece {
   int32_t accumulate;  /* 0 = overwrite, 1 = add */
 } neo_piece;
 int neo_copy_pieces(int64_t rows, const neo_piece* pieces, int32_t num_pieces,
+                    int32_t src_dtype, int32_t dst_dtype, void* stream);
+/* The same for pieces cut into 16-byte vectors (on the narrower dtype's
+ * side): chunk c moves, for every row r, the vector at src + r*src_stride to
+ * dst + r*dst_stride (byte addresses / strides, 16-byte aligned), converting.
+ * Chunks are independent (overwrite only, disjoint destinations), so lanes
+ * take them in parallel: used for the many narrow column blocks of the
+ * sharded exchange (comms.py:692-711); accumulating pieces stay ordered in
+ * neo_copy_pieces. */
+typedef struct neo_chunk {
+  uint64_t src;
+  uint64_t dst;
+  int64_t src_stride;  /* bytes */
+  int64_t dst_stride;  /* bytes */
+} neo_chunk;
+int neo_copy_chunks(int64_t rows, const neo_chunk* chunks, int32_t num_chunks,
                     int32_t src_dtype, int32_t dst_dtype, void* stream);
 
 /* ---- block gather (comms.py:292-353 send packing, comms.py:164-172) ----

@@ -89,6 +89,7 @@ SIGNATURES = {
     "neo_permute_workspace_bytes": (SZ, [I32, I32]),
     "neo_permute_blocks": (C.c_int, [I32, I32, I64, P, P, I32, P, P, P, SZ, P]),
     "neo_copy_pieces": (C.c_int, [I64, P, I32, I32, I32, P]),
+    "neo_copy_chunks": (C.c_int, [I64, P, I32, I32, I32, P]),
     "neo_gather_blocks": (C.c_int, [I32, P, P, P, P, I32, P]),
     "neo_check_indices": (C.c_int, [I32, I64, P, P, P, I32, P, P]),
 }

@@ -245,6 +245,32 @@ copy_pieces_kernel(int64_t rows, const neo_piece* __restrict__ pieces, int32_t n
   }
 }
 
+// Narrow pieces lane-parallel: every chunk is one 16-byte vector (on the
+// narrower side) of one piece, with its row stride; warp per row, lanes
+// stride over the chunks, so a row's many narrow pieces (the sharded
+// exchange's per-shard column blocks) keep all lanes storing 16 bytes.
+template <typename S, typename D>
+__global__ void __launch_bounds__(256)
+copy_chunks_kernel(int64_t rows, const neo_chunk* __restrict__ chunks, int32_t num_chunks) {
+  const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
+  const int64_t r = (int64_t)blockIdx.x * 8 + warp;
+  if (r >= rows) return;
+  constexpr int kMin = sizeof(S) < sizeof(D) ? sizeof(S) : sizeof(D);
+  constexpr int V = 16 / kMin;
+  for (int c = lane; c < num_chunks; c += kWarp) {
+    const neo_chunk ch = chunks[c];
+    const S* src = reinterpret_cast<const S*>(ch.src + r * ch.src_stride);
+    D* dst = reinterpret_cast<D*>(ch.dst + r * ch.dst_stride);
+    Vec<S, V> a = ld_vec<S, V>(src);
+    Vec<D, V> o;
+#pragma unroll
+    for (int e = 0; e < V; ++e) o.v[e] = Elem<D>::from_f(Elem<S>::to_f(a.v[e]));
+#pragma unroll
+    for (int q = 0; q < (int)(sizeof(D) * V) / 16; ++q)
+      reinterpret_cast<uint4*>(dst)[q] = reinterpret_cast<const uint4*>(&o)[q];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // block gather
 
@@ -507,6 +533,28 @@ int neo_copy_pieces(int64_t rows, const neo_piece* pieces, int32_t num_pieces, i
   else return fail(NEO_E_ARG, "copy_pieces: unsupported dtype pair");
 #undef NEO_PC
   return check_launch("copy_pieces");
+}
+
+int neo_copy_chunks(int64_t rows, const neo_chunk* chunks, int32_t num_chunks, int32_t src_dtype,
+                    int32_t dst_dtype, void* stream) {
+  cudaStream_t s = as_stream(stream);
+  if (rows < 0 || num_chunks < 0) return fail(NEO_E_ARG, "copy_chunks: negative size");
+  if (rows == 0 || num_chunks == 0) return NEO_OK;
+  if (!chunks) return fail(NEO_E_ARG, "copy_chunks: null chunk table");
+  const int64_t blocks = (rows + 7) / 8;
+  if (blocks > INT_MAX) return fail(NEO_E_ARG, "copy_chunks: too many rows");
+  const unsigned g = (unsigned)blocks;
+#define NEO_CC(S, D) copy_chunks_kernel<S, D><<<g, 256, 0, s>>>(rows, chunks, num_chunks)
+  if (src_dtype == NEO_F32 && dst_dtype == NEO_F32) NEO_CC(float, float);
+  else if (src_dtype == NEO_F16 && dst_dtype == NEO_F32) NEO_CC(__half, float);
+  else if (src_dtype == NEO_BF16 && dst_dtype == NEO_F32) NEO_CC(__nv_bfloat16, float);
+  else if (src_dtype == NEO_F32 && dst_dtype == NEO_F16) NEO_CC(float, __half);
+  else if (src_dtype == NEO_F32 && dst_dtype == NEO_BF16) NEO_CC(float, __nv_bfloat16);
+  else if (src_dtype == NEO_F16 && dst_dtype == NEO_F16) NEO_CC(__half, __half);
+  else if (src_dtype == NEO_BF16 && dst_dtype == NEO_BF16) NEO_CC(__nv_bfloat16, __nv_bfloat16);
+  else return fail(NEO_E_ARG, "copy_chunks: unsupported dtype pair (16-bit / 32-bit floats)");
+#undef NEO_CC
+  return check_launch("copy_chunks");
 }
 
 int neo_check_indices(int32_t num_tables, int64_t batch, const int64_t* rows, const int64_t* offsets,

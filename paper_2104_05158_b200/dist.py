@@ -71,7 +71,9 @@ class Comm:
         """Returns a handle with .wait() when async_op (None otherwise)."""
         raise NotImplementedError
 
-    def all_reduce_sum(self, tensors, label: str = "other") -> None:  # pragma: no cover
+    def all_reduce_sum(self, tensors, label: str = "other", async_op: bool = False):  # pragma: no cover
+        """Sum over ranks in place; with async_op a handle with wait() (or None
+        when already done)."""
         raise NotImplementedError
 
 
@@ -98,9 +100,9 @@ class NcclComm(Comm):
         self._count("recv", label, self.ranks[0], (sum(osp) - osp[self.ranks[0]]) * out.element_size())
         return self.dist.all_to_all_single(out, inp, osp, isp, group=self.group, async_op=async_op)
 
-    def all_reduce_sum(self, tensors, label: str = "other") -> None:
+    def all_reduce_sum(self, tensors, label: str = "other", async_op: bool = False):
         self._count("reduced", label, self.ranks[0], tensors[0].numel() * tensors[0].element_size())
-        self.dist.all_reduce(tensors[0], group=self.group)
+        return self.dist.all_reduce(tensors[0], group=self.group, async_op=async_op)
 
 
 class LocalComm(Comm):
@@ -129,7 +131,7 @@ class LocalComm(Comm):
                         self._count("sent", label, w, n * ins[w].element_size())
                         self._count("recv", label, v, n * ins[w].element_size())
 
-    def all_reduce_sum(self, tensors, label: str = "other") -> None:
+    def all_reduce_sum(self, tensors, label: str = "other", async_op: bool = False):
         for w, t in enumerate(tensors):
             self._count("reduced", label, w, t.numel() * t.element_size())
         acc = tensors[0].clone()
@@ -353,15 +355,17 @@ class ShardedEmbedding:
         g = upstream_fn(pooled) if upstream_fn is not None else self._ones_like(st, pooled)
         ev.start("bwd")
         self._pack_grad_sym(st, g)
+        # data-parallel tables first: their dense gradient's all-reduce then
+        # runs (NCCL stream) under the sharded backward
+        dp_handle = self._backward_dp_start(st)
         self.hdl_grad.barrier(channel=1)  # all upstream blocks have landed
         wd = self.widths[me]
         recv = self.sym_grad[:n * wd].view(n, wd) if wd else None
         if st.all_group is not None:
             st.all_group.backward(sc["perm_ids"], sc["perm_off"], n, recv, mode="update", optim=self.optim, lr=lr,
                                   eps=eps, table_counts=sc["shard_counts"])
-        self._backward_dp(st)
         ev.stop("bwd")
-        return pooled
+        return pooled, dp_handle
 
     def _ones_like(self, st: RankState, p: torch.Tensor) -> torch.Tensor:
         g = self._buf(st, "ones", p.numel(), p.dtype)[:p.numel()].view_as(p)
@@ -484,14 +488,15 @@ class ShardedEmbedding:
         self._exchange_inputs(batches)
         ev.stop("inputs")
         if self.transport == "nvlink":
-            pooled = [self._step_nvlink(S[0], lr, eps, upstream_fn, ev)]
+            p0, dp_handle = self._step_nvlink(S[0], lr, eps, upstream_fn, ev)
             if self.lay.dp_tables:
                 ev.start("dp")
-                self.comm.all_reduce_sum([st.dp_dense for st in S], label="dp")
+                if dp_handle is not None:
+                    dp_handle.wait()
                 for st in S:
                     self._dp_update(st, lr, eps)
                 ev.stop("dp")
-            return pooled
+            return [p0]
         ev.start("fwd")
         for st in S:
             self._prepare_forward(st)
@@ -522,17 +527,21 @@ class ShardedEmbedding:
             [[B * self.gwidth[st.rank][g]] * W for st in S],
             [[B * self.gwidth[v][g] for v in range(W)] for st in S], async_op=True, label="grad")
             for g in range(self.G)]
+        dp_handle = None
+        if self.lay.dp_tables:  # the DP all-reduce follows the gradient exchanges, under the sharded updates
+            for st in S:
+                self._backward_dp(st)
+            dp_handle = self.comm.all_reduce_sum([st.dp_dense for st in S], label="dp", async_op=True)
         for g, h in enumerate(handles):  # update of group g while group g+1's gradients arrive
             if h is not None:
                 h.wait()
             for st in S:
                 self._backward_group(st, g, lr, eps)
-        for st in S:
-            self._backward_dp(st)
         ev.stop("bwd")
         if self.lay.dp_tables:
             ev.start("dp")
-            self.comm.all_reduce_sum([st.dp_dense for st in S], label="dp")
+            if dp_handle is not None:
+                dp_handle.wait()
             for st in S:
                 self._dp_update(st, lr, eps)
             ev.stop("dp")
@@ -805,6 +814,15 @@ class ShardedEmbedding:
             st.dp_dense.zero_()
             st.dp_group.backward(sc["dp_ids"], sc["dp_off"], self.B, sc["dp_grad"], mode="dense",
                                  dense_grads=st.dp_dense_views, table_counts=sc["dp_counts"])
+
+    def _backward_dp_start(self, st: RankState):
+        """One rank's data-parallel dense gradient, then its all-reduce issued
+        asynchronously (one process per GPU); the caller waits before the
+        update."""
+        if not self.lay.dp_tables:
+            return None
+        self._backward_dp(st)
+        return self.comm.all_reduce_sum([st.dp_dense], label="dp", async_op=True)
 
     def _dp_update(self, st: RankState, lr: float, eps: float) -> None:
         for w, m, g in zip(st.dp_group.weights, st.dp_group.moments, st.dp_dense_views):

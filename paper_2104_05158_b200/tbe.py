@@ -591,24 +591,71 @@ class Piece:
     accumulate: bool = False
 
 
-def copy_pieces(rows: int, pieces: Sequence[Piece], pieces_dev: Optional[torch.Tensor] = None) -> None:
-    """Apply pieces in order to rows [0, rows) (neo_copy_pieces)."""
+class PackedPieces:
+    """Device tables of a piece list: pieces cut into independent 16-byte
+    chunks (neo_copy_chunks, lane-parallel) and the pieces that must stay
+    ordered (accumulating ones and anything not 16-byte aligned)."""
+
+    def __init__(self, chunks: Optional[torch.Tensor], n_chunks: int, rest: Optional[torch.Tensor], n_rest: int,
+                 sd, dd):
+        self.chunks, self.n_chunks, self.rest, self.n_rest, self.sd, self.dd = chunks, n_chunks, rest, n_rest, sd, dd
+
+
+def copy_pieces(rows: int, pieces: Sequence[Piece], pieces_dev=None) -> None:
+    """Apply pieces to rows [0, rows) (neo_copy_chunks + neo_copy_pieces):
+    the same result as applying them in array order, given that overwriting
+    pieces have disjoint destinations."""
     if not pieces:
         return
-    sd, dd = pieces[0].src.dtype, pieces[0].dst.dtype
     if pieces_dev is None:
         pieces_dev = pack_pieces(pieces, pieces[0].src.device)
-    capi.check(capi.lib().neo_copy_pieces(rows, pieces_dev.data_ptr(), len(pieces), DTYPE_CODE[sd],
-                                          DTYPE_CODE[dd], _stream()), "neo_copy_pieces")
+    pk = pieces_dev
+    if pk.n_chunks:
+        capi.check(capi.lib().neo_copy_chunks(rows, pk.chunks.data_ptr(), pk.n_chunks, DTYPE_CODE[pk.sd],
+                                              DTYPE_CODE[pk.dd], _stream()), "neo_copy_chunks")
+    if pk.n_rest:
+        capi.check(capi.lib().neo_copy_pieces(rows, pk.rest.data_ptr(), pk.n_rest, DTYPE_CODE[pk.sd],
+                                              DTYPE_CODE[pk.dd], _stream()), "neo_copy_pieces")
 
 
-def pack_pieces(pieces: Sequence[Piece], device) -> torch.Tensor:
-    arr = (capi.NeoPiece * len(pieces))()
-    for i, p in enumerate(pieces):
-        arr[i] = capi.NeoPiece(p.src.data_ptr(), p.dst.data_ptr(), p.src.stride(0), p.dst.stride(0),
-                               p.src_col, p.dst_col, p.width, int(p.accumulate))
-    raw = np.frombuffer(bytes(arr), dtype=np.uint8).copy()
-    return torch.from_numpy(raw).to(device)
+def _pieces_disjoint(pieces: Sequence[Piece]) -> bool:
+    by_dst = {}
+    for p in pieces:
+        if not p.accumulate:
+            by_dst.setdefault((p.dst.data_ptr(), p.dst.stride(0)), []).append((p.dst_col, p.dst_col + p.width))
+    for iv in by_dst.values():
+        iv.sort()
+        if any(b[0] < a[1] for a, b in zip(iv, iv[1:])):
+            return False
+    return True
+
+
+def pack_pieces(pieces: Sequence[Piece], device) -> PackedPieces:
+    sd, dd = pieces[0].src.dtype, pieces[0].dst.dtype
+    es, ed = pieces[0].src.element_size(), pieces[0].dst.element_size()
+    V = 16 // min(es, ed)
+    flat_ok = es <= 4 and ed <= 4 and _pieces_disjoint(pieces)
+    chunks, rest = [], []
+    for p in pieces:
+        sa, da = p.src.data_ptr() + p.src_col * es, p.dst.data_ptr() + p.dst_col * ed
+        ss, ds = p.src.stride(0) * es, p.dst.stride(0) * ed
+        if (flat_ok and not p.accumulate and p.width % V == 0 and sa % 16 == 0 and da % 16 == 0
+                and ss % 16 == 0 and ds % 16 == 0):
+            for j in range(0, p.width, V):
+                chunks.append((sa + j * es, da + j * ed, ss, ds))
+        else:
+            rest.append(p)
+    ch = None
+    if chunks:
+        ch = torch.from_numpy(np.array(chunks, dtype=np.uint64).view(np.int64)).to(device)
+    arr = None
+    if rest:
+        a = (capi.NeoPiece * len(rest))()
+        for i, p in enumerate(rest):
+            a[i] = capi.NeoPiece(p.src.data_ptr(), p.dst.data_ptr(), p.src.stride(0), p.dst.stride(0),
+                                 p.src_col, p.dst_col, p.width, int(p.accumulate))
+        arr = torch.from_numpy(np.frombuffer(bytes(a), dtype=np.uint8).copy()).to(device)
+    return PackedPieces(ch, len(chunks), arr, len(rest), sd, dd)
 
 
 def gather_blocks(srcs: Sequence[torch.Tensor], counts: Sequence[int], dst: torch.Tensor) -> torch.Tensor:

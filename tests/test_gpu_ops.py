@@ -301,6 +301,7 @@ def test_backward_subgroup_split_bitwise(pkg, monkeypatch):
     from paper_2104_05158_b200 import tbe
 
     monkeypatch.setattr(tbe, "SORT_BITS", 13)  # 8192 rows per sub-group
+    monkeypatch.setenv("NEO_BWD_VARIANT", "pipe")  # the sorted path both times (sub-groups split its sort)
     rng = np.random.default_rng(21)
     rows, dims, B = [3000, 5000, 2000, 7000, 100], [128] * 5, 512
     lengths, idx = _random_group_case(rng, 5, rows, dims, B, 20)

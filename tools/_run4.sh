@@ -1,6 +1,6 @@
-timeout 1200 python -m pytest tests/test_gpu_sharded.py tests/test_gpu_bytes.py tests/test_gpu_configs.py tests/test_gpu_dist.py tests/test_gpu_dropin.py tests/test_gpu_bucket.py -x -q 2>&1 | tail -4
+timeout 1200 python -m pytest tests/test_gpu_sharded.py tests/test_gpu_bytes.py tests/test_gpu_dist.py tests/test_gpu_ops.py -x -q 2>&1 | tail -4
 R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 4"
-for w in c5; do
+for w in c5 c3; do
   $R --workload $w --steps 12 --warmup 3 > gpurun_out/n4_${w}.json 2>gpurun_out/n4_${w}.err; python tools/bline.py $w < gpurun_out/n4_${w}.json
   python - <<PY
 import json
