@@ -332,6 +332,22 @@ int neo_tier_prepare(int64_t num_rows, int64_t num_sets, int32_t ways, const voi
                      void* cache_moments, void* host_weights, void* host_moments, int64_t row_bytes,
                      int64_t moment_bytes, int32_t* slots_out, int64_t* counters, void* workspace,
                      size_t workspace_bytes, neo_error* err, void* stream);
+/* neo_tier_prepare with set-overflow spill: an access whose set has no free
+ * way this batch (more than `ways` distinct rows of the set in the batch)
+ * takes one of spill_cap extra slots after the cache (slot num_sets*ways + k;
+ * cache_weights / cache_moments must hold them), fetched like a miss; its
+ * (slot, row) pair goes to spill_list[2k..2k+1] and counters[4] counts the
+ * spills (counters: 5 int64).  neo_tier_spill_writeback, issued after the
+ * backward, writes the spilled rows (and their optimizer state) back to host.
+ * Only spills beyond spill_cap map to slot -1 (counters[2]). */
+int neo_tier_prepare_spill(int64_t num_rows, int64_t num_sets, int32_t ways, const void* ids, int32_t index_dtype,
+                           int64_t num_ids, int64_t* tags, uint32_t* stamps, uint32_t stamp, void* cache_weights,
+                           void* cache_moments, void* host_weights, void* host_moments, int64_t row_bytes,
+                           int64_t moment_bytes, int32_t* slots_out, int64_t* counters, int64_t spill_cap,
+                           int64_t* spill_list, void* workspace, size_t workspace_bytes, neo_error* err, void* stream);
+int neo_tier_spill_writeback(const int64_t* spill_list, const int64_t* counters, int64_t spill_cap,
+                             const void* cache_weights, const void* cache_moments, void* host_weights,
+                             void* host_moments, int64_t row_bytes, int64_t moment_bytes, void* stream);
 int neo_tier_flush(int64_t num_slots, const int64_t* tags, const void* cache_weights, const void* cache_moments,
                    void* host_weights, void* host_moments, int64_t row_bytes, int64_t moment_bytes, void* stream);
 

@@ -64,6 +64,9 @@ SIGNATURES = {
     "neo_tier_prepare": (C.c_int, [I64, I64, I32, P, I32, I64, P, P, C.c_uint32, P, P, P, P, I64, I64, P, P, P, SZ,
                                    P, P]),
     "neo_tier_flush": (C.c_int, [I64, P, P, P, P, P, I64, I64, P]),
+    "neo_tier_prepare_spill": (C.c_int, [I64, I64, I32, P, I32, I64, P, P, C.c_uint32, P, P, P, P, I64, I64, P, P,
+                                         I64, P, P, SZ, P, P]),
+    "neo_tier_spill_writeback": (C.c_int, [P, P, I64, P, P, P, P, I64, I64, P]),
     "neo_tbe_forward_scatter": (
         C.c_int,
         [I32, I64, P, P, I32, P, I32, P, I32, P, I32, P, I64, I32, I64, P, P],

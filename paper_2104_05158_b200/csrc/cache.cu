@@ -314,7 +314,7 @@ tier_assign_kernel(const Idx* __restrict__ ids, const int32_t* __restrict__ pos,
                    const int64_t* __restrict__ num_segs, int64_t n, int64_t H, int64_t num_sets, int32_t ways,
                    int64_t* __restrict__ tags, uint32_t* __restrict__ stamps, uint32_t stamp,
                    int32_t* __restrict__ slots_out, int64_t* __restrict__ xfer,
-                   unsigned long long* __restrict__ counters) {
+                   unsigned long long* __restrict__ counters, int64_t spill_cap, int64_t* __restrict__ spill_list) {
   const unsigned full = 0xffffffffu;
   const int lane = threadIdx.x % kWarp;
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
@@ -330,6 +330,11 @@ tier_assign_kernel(const Idx* __restrict__ ids, const int32_t* __restrict__ pos,
     const int64_t base = set_id * ways;
     int64_t tag = lane < ways ? tags[base + lane] : -2;
     uint32_t st = lane < ways ? stamps[base + lane] : 0xffffffffu;
+    // rows of this set that found no free way this batch: one spill slot each
+    // (lane k holds the k-th), fetched now, written back after the backward
+    int64_t sp_tag = -1;
+    int32_t sp_slot = -1;
+    int sp_n = 0;
     // pass 1: stamp the ways this batch uses (lane-parallel: the 32 accesses
     // of a window against each way's tag)
     for (int64_t j0 = s0; j0 < s1; j0 += kWarp) {
@@ -376,9 +381,41 @@ tier_assign_kernel(const Idx* __restrict__ ids, const int32_t* __restrict__ pos,
         }
         const bool cand = lane < ways && st != stamp;
         const unsigned cm = __ballot_sync(full, cand);
-        if (!cm) {
-          ++over;
-          if (lane == 0) slots_out[p] = -1;
+        if (!cm) {  // set overflow: a spill slot for the batch
+          const unsigned sm = __ballot_sync(full, sp_tag == r);
+          if (sm) {
+            prev_slot = __shfl_sync(full, sp_slot, __ffs(sm) - 1);
+            if (lane == 0) slots_out[p] = prev_slot;
+            continue;
+          }
+          long long idx = -1;
+          if (lane == 0 && sp_n < kWarp && spill_cap > 0) {
+            idx = (long long)atomicAdd(counters + 4, 1ull);
+            if (idx >= spill_cap) idx = -1;
+          }
+          idx = __shfl_sync(full, idx, 0);
+          if (idx < 0) {
+            ++over;
+            if (lane == 0) slots_out[p] = -1;
+            continue;
+          }
+          const int32_t slot = (int32_t)(num_sets * ways + idx);
+          if (lane == sp_n) {
+            sp_tag = r;
+            sp_slot = slot;
+          }
+          ++sp_n;
+          ++misses;
+          prev_slot = slot;
+          if (lane == 0) {
+            spill_list[2 * idx] = slot;
+            spill_list[2 * idx + 1] = r;
+            const unsigned long long x = atomicAdd(counters + 3, 1ull);
+            xfer[3 * x + 0] = slot;
+            xfer[3 * x + 1] = -1;  // nothing to write back now
+            xfer[3 * x + 2] = r;
+            slots_out[p] = slot;
+          }
           continue;
         }
         const uint32_t smin = __reduce_min_sync(full, cand ? st : 0xffffffffu);
@@ -496,6 +533,21 @@ tier_flush_kernel(int64_t num_slots, const int64_t* __restrict__ tags, const uns
   }
 }
 
+__global__ void __launch_bounds__(256)
+tier_spill_writeback_kernel(const int64_t* __restrict__ spill_list, const unsigned long long* __restrict__ counters,
+                            int64_t spill_cap, const unsigned char* cache_w, const unsigned char* cache_m,
+                            unsigned char* host_w, unsigned char* host_m, int64_t row_bytes, int64_t mom_bytes) {
+  const int lane = threadIdx.x % kWarp;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kWarp;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) / kWarp;
+  const int64_t n = min64((int64_t)counters[4], spill_cap);
+  for (int64_t i = warp; i < n; i += nwarps) {
+    const int64_t slot = spill_list[2 * i], r = spill_list[2 * i + 1];
+    warp_copy(host_w + r * row_bytes, cache_w + slot * row_bytes, row_bytes, lane);
+    if (mom_bytes) warp_copy(host_m + r * mom_bytes, cache_m + slot * mom_bytes, mom_bytes, lane);
+  }
+}
+
 static size_t tier_ws(int64_t n) { return cache_ws(n) + a256(3 * 8 * (size_t)n); }
 
 static unsigned sm_grid(int64_t warps_wanted) {
@@ -510,13 +562,32 @@ static unsigned sm_grid(int64_t warps_wanted) {
 
 extern "C" size_t neo_tier_workspace_bytes(int64_t num_ids) { return neo::tier_ws(num_ids < 1 ? 1 : num_ids); }
 
+extern "C" int neo_tier_prepare_spill(int64_t num_rows, int64_t num_sets, int32_t ways, const void* ids,
+                                      int32_t index_dtype, int64_t num_ids, int64_t* tags, uint32_t* stamps,
+                                      uint32_t stamp, void* cache_weights, void* cache_moments, void* host_weights,
+                                      void* host_moments, int64_t row_bytes, int64_t moment_bytes,
+                                      int32_t* slots_out, int64_t* counters, int64_t spill_cap, int64_t* spill_list,
+                                      void* workspace, size_t workspace_bytes, neo_error* err, void* stream);
+
 extern "C" int neo_tier_prepare(int64_t num_rows, int64_t num_sets, int32_t ways, const void* ids,
                                 int32_t index_dtype, int64_t num_ids, int64_t* tags, uint32_t* stamps,
                                 uint32_t stamp, void* cache_weights, void* cache_moments, void* host_weights,
                                 void* host_moments, int64_t row_bytes, int64_t moment_bytes, int32_t* slots_out,
                                 int64_t* counters, void* workspace, size_t workspace_bytes, neo_error* err,
                                 void* stream) {
+  return neo_tier_prepare_spill(num_rows, num_sets, ways, ids, index_dtype, num_ids, tags, stamps, stamp,
+                                cache_weights, cache_moments, host_weights, host_moments, row_bytes, moment_bytes,
+                                slots_out, counters, 0, nullptr, workspace, workspace_bytes, err, stream);
+}
+
+extern "C" int neo_tier_prepare_spill(int64_t num_rows, int64_t num_sets, int32_t ways, const void* ids,
+                                      int32_t index_dtype, int64_t num_ids, int64_t* tags, uint32_t* stamps,
+                                      uint32_t stamp, void* cache_weights, void* cache_moments, void* host_weights,
+                                      void* host_moments, int64_t row_bytes, int64_t moment_bytes,
+                                      int32_t* slots_out, int64_t* counters, int64_t spill_cap, int64_t* spill_list,
+                                      void* workspace, size_t workspace_bytes, neo_error* err, void* stream) {
   using namespace neo;
+  if (spill_cap < 0 || (spill_cap > 0 && !spill_list)) return fail(NEO_E_ARG, "neo_tier_prepare: spill list");
   cudaStream_t s = as_stream(stream);
   if (num_rows < 1 || num_sets < 1 || num_sets > (int64_t)UINT32_MAX) return fail(NEO_E_ARG, "num_sets/num_rows");
   if (ways < 1 || ways > kWarp) return fail(NEO_E_ARG, "ways: 1..32 (one way per lane)");
@@ -526,7 +597,7 @@ extern "C" int neo_tier_prepare(int64_t num_rows, int64_t num_sets, int32_t ways
     return fail(NEO_E_ARG, "row/moment bytes must be multiples of 4; stamp >= 1");
   if (!tags || !stamps || !cache_weights || !host_weights || !slots_out || !counters)
     return fail(NEO_E_ARG, "neo_tier_prepare: null pointer");
-  if (cudaMemsetAsync(counters, 0, 4 * sizeof(int64_t), s) != cudaSuccess)
+  if (cudaMemsetAsync(counters, 0, (spill_cap > 0 ? 5 : 4) * sizeof(int64_t), s) != cudaSuccess)
     return fail(NEO_E_CUDA, "neo_tier_prepare: memset failed");
   const int64_t n = num_ids;
   if (n == 0) return NEO_OK;
@@ -562,10 +633,12 @@ extern "C" int neo_tier_prepare(int64_t num_rows, int64_t num_sets, int32_t ways
   const unsigned agrid = sm_grid(min64(n, num_sets));
   if (index_dtype == NEO_I32)
     tier_assign_kernel<int32_t><<<agrid, 256, 0, s>>>((const int32_t*)ids, vbuf.Current(), starts, nseg, n, num_rows,
-                                                       num_sets, ways, tags, stamps, stamp, slots_out, xfer, cnt);
+                                                       num_sets, ways, tags, stamps, stamp, slots_out, xfer, cnt,
+                                                       spill_cap, spill_list);
   else
     tier_assign_kernel<int64_t><<<agrid, 256, 0, s>>>((const int64_t*)ids, vbuf.Current(), starts, nseg, n, num_rows,
-                                                       num_sets, ways, tags, stamps, stamp, slots_out, xfer, cnt);
+                                                       num_sets, ways, tags, stamps, stamp, slots_out, xfer, cnt,
+                                                       spill_cap, spill_list);
   rc = check_launch("neo_tier_prepare(assign)");
   if (rc) return rc;
   tier_transfer_kernel<<<sm_grid(n), 256, 0, s>>>(xfer, cnt, (unsigned char*)cache_weights,
@@ -585,4 +658,19 @@ extern "C" int neo_tier_flush(int64_t num_slots, const int64_t* tags, const void
       num_slots, tags, (const unsigned char*)cache_weights, (const unsigned char*)cache_moments,
       (unsigned char*)host_weights, (unsigned char*)host_moments, row_bytes, moment_bytes);
   return check_launch("neo_tier_flush");
+}
+
+extern "C" int neo_tier_spill_writeback(const int64_t* spill_list, const int64_t* counters, int64_t spill_cap,
+                                        const void* cache_weights, const void* cache_moments, void* host_weights,
+                                        void* host_moments, int64_t row_bytes, int64_t moment_bytes, void* stream) {
+  using namespace neo;
+  if (spill_cap < 0 || row_bytes < 4 || (row_bytes & 3) || (moment_bytes & 3))
+    return fail(NEO_E_ARG, "neo_tier_spill_writeback: bad sizes");
+  if (spill_cap == 0) return NEO_OK;
+  if (!spill_list || !counters) return fail(NEO_E_ARG, "neo_tier_spill_writeback: null pointer");
+  tier_spill_writeback_kernel<<<sm_grid(spill_cap), 256, 0, as_stream(stream)>>>(
+      spill_list, reinterpret_cast<const unsigned long long*>(counters), spill_cap,
+      (const unsigned char*)cache_weights, (const unsigned char*)cache_moments, (unsigned char*)host_weights,
+      (unsigned char*)host_moments, row_bytes, moment_bytes);
+  return check_launch("neo_tier_spill_writeback");
 }

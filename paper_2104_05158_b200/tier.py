@@ -29,9 +29,14 @@ from .tbe import INDEX_CODE, WORKSPACE, ErrorRecord, TableGroup, _stream, raise_
 
 
 class TieredTableGroup:
+    """spill: extra HBM slots per table for rows of sets that overflow their
+    ways within one batch (default: ways x 256); they are fetched like misses
+    and written back after the backward.  Only a batch that also exhausts
+    the spill slots raises InvalidValue."""
+
     def __init__(self, rows: Sequence[int], dims: Sequence[int], num_sets, ways: int = 32,
                  dtype=torch.float32, optim: str = "rowwise_adagrad", device=None,
-                 table_ids: Optional[Sequence[str]] = None):
+                 table_ids: Optional[Sequence[str]] = None, spill: Optional[int] = None):
         if ways < 1 or ways > 32:
             raise InvalidValue("ways", "1..32 (one way per lane)")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -40,7 +45,13 @@ class TieredTableGroup:
         self.ways, self.optim, self.dtype = ways, optim, dtype
         self.table_ids = list(table_ids) if table_ids else [f"t{i}" for i in range(self.T)]
         slots = [s * ways for s in self.num_sets]
-        self.cache = TableGroup(slots, self.dims, dtype=dtype, optim=optim, device=self.device)
+        self.spill = int(ways * 256 if spill is None else spill)
+        if self.spill < 0:
+            raise InvalidValue("spill", "must be >= 0")
+        self.cache = TableGroup([n + self.spill for n in slots], self.dims, dtype=dtype, optim=optim,
+                                device=self.device)
+        self.spill_lists = [torch.zeros(2 * max(self.spill, 1), dtype=torch.int64, device=self.device)
+                            for _ in range(self.T)]
         esz = torch.empty(0, dtype=dtype).element_size()
         self.row_bytes = [d * esz for d in self.dims]
         acc = self.cache.acc
@@ -57,15 +68,17 @@ class TieredTableGroup:
         self.tags = [torch.full((n,), -1, dtype=torch.int64, device=self.device) for n in slots]
         self.stamps = [torch.zeros(n, dtype=torch.int32, device=self.device) for n in slots]
         self.stamp = 0
-        self.counters = torch.zeros((self.T, 4), dtype=torch.int64, device=self.device)
-        self.stats = {"misses": 0, "writebacks": 0, "accesses": 0}
+        self.counters = torch.zeros((self.T, 5), dtype=torch.int64, device=self.device)
+        self.stats = {"misses": 0, "writebacks": 0, "accesses": 0, "spills": 0}
         self._slots = None
 
     # ------------------------------------------------------------------
     def map_batch(self, indices: torch.Tensor, table_counts: Sequence[int], err: Optional[ErrorRecord] = None):
         """Slot ids (int32, the layout of `indices`) of one batch; fetches and
-        writes back rows as needed.  Raises InvalidValue when a set needs more
-        than `ways` rows in one batch, IndexOutOfRange on a bad id."""
+        writes back rows as needed.  Rows of a set that needs more than `ways`
+        rows in this batch take spill slots (up to 32 per set, `spill` per
+        table); InvalidValue only when those run out, IndexOutOfRange on a bad
+        id."""
         self.stamp += 1
         n = int(indices.numel())
         slots = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
@@ -79,20 +92,22 @@ class TieredTableGroup:
                 continue
             ws = WORKSPACE.get("tier", capi.lib().neo_tier_workspace_bytes(cnt), self.device)
             m = self.cache.moments[t]
-            rc = capi.lib().neo_tier_prepare(
+            rc = capi.lib().neo_tier_prepare_spill(
                 self.rows[t], self.num_sets[t], self.ways, indices.data_ptr() + int(off[t]) * isz,
                 INDEX_CODE[indices.dtype], cnt, self.tags[t].data_ptr(), self.stamps[t].data_ptr(), self.stamp,
                 self.cache.weights[t].data_ptr(), None if m is None else m.data_ptr(), self.host_w[t].data_ptr(),
                 None if self.host_m[t] is None else self.host_m[t].data_ptr(), self.row_bytes[t], self.mom_bytes[t],
-                slots.data_ptr() + int(off[t]) * 4, self.counters[t].data_ptr(), ws.data_ptr(), ws.numel(),
-                err.ptr, _stream())
-            capi.check(rc, "neo_tier_prepare")
+                slots.data_ptr() + int(off[t]) * 4, self.counters[t].data_ptr(), self.spill,
+                self.spill_lists[t].data_ptr(), ws.data_ptr(), ws.numel(), err.ptr, _stream())
+            capi.check(rc, "neo_tier_prepare_spill")
         c = self.counters.cpu().numpy()
         if own_err:
             raise_if_bad(err, self.table_ids)
         if c[:, 2].sum() > 0:
             raise InvalidValue("num_sets", f"{int(c[:, 2].sum())} accesses found no free way: a set needs more than "
-                                           f"{self.ways} rows in one batch")
+                                           f"{self.ways} rows in one batch and the {self.spill} spill slots "
+                                           "(or 32 per set) are used up")
+        self.stats["spills"] += int(c[:, 4].sum())
         self.stats["misses"] += int(c[:, 0].sum())
         self.stats["writebacks"] += int(c[:, 1].sum())
         self.stats["accesses"] += n
@@ -111,6 +126,13 @@ class TieredTableGroup:
             raise InvalidValue("backward", "no mapped batch: call forward() first")
         self.cache.backward(self._slots, offsets, batch, grad, mode="update", optim=optim or self.optim, lr=lr,
                             eps=eps, table_counts=table_counts)
+        for t in range(self.T):  # spilled rows go home (their slots are per-batch)
+            m = self.cache.moments[t]
+            capi.check(capi.lib().neo_tier_spill_writeback(
+                self.spill_lists[t].data_ptr(), self.counters[t].data_ptr(), self.spill,
+                self.cache.weights[t].data_ptr(), None if m is None else m.data_ptr(), self.host_w[t].data_ptr(),
+                None if self.host_m[t] is None else self.host_m[t].data_ptr(), self.row_bytes[t], self.mom_bytes[t],
+                _stream()), "neo_tier_spill_writeback")
 
     def flush(self) -> None:
         """Write every cached row (and its optimizer state) back to host memory."""

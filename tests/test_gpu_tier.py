@@ -82,12 +82,59 @@ def test_tier_training_matches_full_hbm(mods, dtype, optim, zipf):
 
 def test_tier_errors(mods):
     tbe, tier = mods
-    tg = tier.TieredTableGroup([1000], [32], num_sets=1, ways=2)
+    tg = tier.TieredTableGroup([1000], [32], num_sets=1, ways=2, spill=0)
     off = torch.tensor([0, 4], dtype=torch.int64, device="cuda")
-    with pytest.raises(tier.InvalidValue):  # one set, 2 ways, 3 distinct rows in one batch
+    with pytest.raises(tier.InvalidValue):  # one set, 2 ways, 3 distinct rows in one batch, no spill slots
         tg.forward(torch.tensor([1, 2, 3, 1], dtype=torch.int32, device="cuda"), off, 1, [4])
+    tg.spill_ok = tier.TieredTableGroup([1000], [32], num_sets=1, ways=2)  # default spill slots: served
+    assert tg.spill_ok.forward(torch.tensor([1, 2, 3, 1], dtype=torch.int32, device="cuda"), off, 1, [4]).shape == (1, 32)
+    assert tg.spill_ok.stats["spills"] == 1
     tg2 = tier.TieredTableGroup([1000], [32], num_sets=8, ways=4, table_ids=["emb"])
     import paper_2104_05158_b200 as p
 
     with pytest.raises(p.IndexOutOfRange):
         tg2.forward(torch.tensor([1, 2, 1000, 1], dtype=torch.int32, device="cuda"), off, 1, [4])
+
+
+@pytest.mark.parametrize("optim", ["rowwise_adagrad", "adagrad"])
+def test_tier_set_overflow_spills_and_matches_full_hbm(mods, optim):
+    """A cache far too small for one batch (4 ways, 128 sets: every set sees
+    ~15 distinct rows per batch): the overflowing rows take spill slots, are
+    fetched, updated and written back; training stays bitwise equal to the
+    full-HBM tables (uniform ids)."""
+    tbe, tier = mods
+    rows, dims, B, L, steps = [40000, 9000], [64, 32], 256, 8, 3
+    T = len(rows)
+    rng = np.random.default_rng(23)
+    init = [rng.standard_normal((r, d)).astype(np.float32) for r, d in zip(rows, dims)]
+    full = tbe.TableGroup(rows, dims, dtype=torch.float32, optim=optim)
+    for w, v in zip(full.weights, init):
+        w.copy_(torch.from_numpy(v))
+    tg = tier.TieredTableGroup(rows, dims, num_sets=128, ways=4, optim=optim, spill=4096)
+    for t in range(T):
+        tg.host_w[t].copy_(torch.from_numpy(init[t]))
+    counts = [B * L] * T
+    off = torch.arange(0, T * B + 1, dtype=torch.int64, device="cuda") * L
+    for s in range(steps):
+        ix = torch.from_numpy(np.concatenate([rng.integers(0, r, B * L) for r in rows]).astype(np.int32)).cuda()
+        up = torch.from_numpy(rng.standard_normal((B, sum(dims))).astype(np.float32)).cuda()
+        a = full.forward(ix, off, B)
+        b = tg.forward(ix, off, B, counts)
+        assert torch.equal(a, b), f"pooled outputs differ at step {s}"
+        full.backward(ix, off, B, up, mode="update", optim=optim, lr=0.05, eps=1e-8, table_counts=counts)
+        tg.backward(off, B, up, counts, lr=0.05, eps=1e-8)
+    tg.flush()
+    assert tg.stats["spills"] > 1000
+    for t in range(T):
+        assert torch.equal(full.weights[t].cpu(), tg.host_w[t]), f"table {t} values"
+        assert torch.equal(full.moments[t].cpu(), tg.host_m[t]), f"table {t} optimizer state"
+
+
+def test_tier_spill_exhausted_raises(mods):
+    tbe, tier = mods
+    tg = tier.TieredTableGroup([5000], [32], num_sets=2, ways=2, spill=8)
+    ix = torch.arange(0, 2048, dtype=torch.int32, device="cuda")
+    off = torch.tensor([0, 2048], dtype=torch.int64, device="cuda")
+    from paper_2104_05158_b200.errors import InvalidValue
+    with pytest.raises(InvalidValue):
+        tg.forward(ix, off, 1, [2048])
