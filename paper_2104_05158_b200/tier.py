@@ -145,3 +145,87 @@ class TieredTableGroup:
                                            self.row_bytes[t], self.mom_bytes[t], _stream())
             capi.check(rc, "neo_tier_flush")
         torch.cuda.current_stream(self.device).synchronize()
+
+
+class HybridTableGroup:
+    """Tables larger than HBM, split by rows (the reference's "hbm+dram"
+    worker tier, planner.py:512-522): rows [0, hbm_rows[t]) of table t live
+    in HBM (a TableGroup), the rest in host memory behind the slot cache
+    (TieredTableGroup).  A batch is bucketised into the two row ranges in one
+    launch (neo_bucketize_rowwise_multi), (table, part, bag) blocks are
+    permuted to (part, table, bag) (neo_permute_blocks), each part runs the
+    unchanged TBE kernels, and the pooled rows are the two partial sums added
+    in part order, exactly as a row-wise table with two shards
+    (comms.py:692-711).  Every row lives in one part and sees its
+    occurrences in batch order, so updated weights and optimizer state are
+    bitwise those of the whole table in HBM."""
+
+    def __init__(self, rows: Sequence[int], dims: Sequence[int], hbm_rows: Sequence[int], num_sets, ways: int = 32,
+                 dtype=torch.float32, optim: str = "rowwise_adagrad", device=None, spill: Optional[int] = None):
+        self.rows, self.dims, self.T = [int(r) for r in rows], [int(d) for d in dims], len(rows)
+        self.hbm_rows = [int(h) for h in hbm_rows]
+        if any(not 0 < h < r for h, r in zip(self.hbm_rows, self.rows)):
+            raise InvalidValue("hbm_rows", "each table needs rows in both parts (0 < hbm_rows < rows)")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.optim = optim
+        self.hbm = TableGroup(self.hbm_rows, self.dims, dtype=dtype, optim=optim, device=self.device)
+        self.host = TieredTableGroup([r - h for r, h in zip(self.rows, self.hbm_rows)], self.dims, num_sets, ways,
+                                     dtype=dtype, optim=optim, device=self.device, spill=spill)
+        st = np.zeros((self.T, 3), dtype=np.int64)
+        st[:, 1] = self.hbm_rows
+        st[:, 2] = self.rows
+        self._tables = torch.arange(self.T, dtype=torch.int32, device=self.device)
+        self._starts = torch.from_numpy(st.reshape(-1)).to(self.device)
+        self._k = torch.full((self.T,), 2, dtype=torch.int32, device=self.device)
+        self._parts = None
+
+    def _split(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int):
+        T, B, dev = self.T, batch, self.device
+        lens = torch.empty(T * 2 * B, dtype=torch.int64, device=dev)
+        offs = torch.empty(T * 2 * B + 1, dtype=torch.int64, device=dev)
+        idx = torch.empty(max(int(indices.numel()), 1), dtype=indices.dtype, device=dev)
+        ws = WORKSPACE.get("bucketize", capi.lib().neo_bucketize_workspace_bytes(T * B, 2), dev)
+        capi.check(capi.lib().neo_bucketize_rowwise_multi(
+            T, B, self._tables.data_ptr(), offsets.data_ptr(), indices.data_ptr(), INDEX_CODE[indices.dtype], 2,
+            self._starts.data_ptr(), self._k.data_ptr(), lens.data_ptr(), offs.data_ptr(), idx.data_ptr(),
+            ws.data_ptr(), ws.numel(), _stream()), "neo_bucketize_rowwise_multi")
+        # (table, part, bag) -> (part, table, bag): each part's ids table-major
+        from .tbe import lengths_to_offsets, permute_blocks
+        plen, pidx = permute_blocks(T, 2, B, lens, idx)
+        plen = plen.view(2, T * B)
+        cnt = plen.view(2, T, B).sum(dim=2).cpu().numpy()  # host counts per (part, table)
+        n0 = int(cnt[0].sum())
+        off0 = lengths_to_offsets(plen[0])
+        off1 = lengths_to_offsets(plen[1])
+        return (pidx[:max(n0, 1)], off0, cnt[0].tolist()), (pidx[n0:], off1, cnt[1].tolist())
+
+    def forward(self, indices: torch.Tensor, offsets: torch.Tensor, batch: int,
+                out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """Pooled (batch, sum D) outputs: HBM part + host part, in that order.
+        offsets: int64 over T * batch bags (table-major, the CombinedBatch layout)."""
+        p0, p1 = self._split(indices, offsets, batch)
+        self._parts = (p0, p1)
+        out = self.hbm.forward(p0[0], p0[1], batch, out=out)
+        out += self.host.forward(p1[0], p1[1], batch, p1[2])
+        return out
+
+    def backward(self, batch: int, grad: torch.Tensor, lr: float, eps: float) -> None:
+        """Fused backward + optimizer of both parts for the last forward()."""
+        if self._parts is None:
+            raise InvalidValue("backward", "no split batch: call forward() first")
+        (i0, o0, c0), (_, o1, c1) = self._parts
+        self.hbm.backward(i0, o0, batch, grad, mode="update", optim=self.optim, lr=lr, eps=eps, table_counts=c0)
+        self.host.backward(o1, batch, grad, c1, lr=lr, eps=eps)
+
+    def flush(self) -> None:
+        self.host.flush()
+
+    def row(self, t: int, r: int):
+        """(weight row, optimizer state) of table t's row r, wherever it lives
+        (call flush() first for host rows)."""
+        h = self.hbm_rows[t]
+        if r < h:
+            m = self.hbm.moments[t]
+            return self.hbm.weights[t][r].cpu(), None if m is None else m[r].cpu()
+        m = self.host.host_m[t]
+        return self.host.host_w[t][r - h], None if m is None else m[r - h]

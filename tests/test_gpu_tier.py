@@ -138,3 +138,45 @@ def test_tier_spill_exhausted_raises(mods):
     from paper_2104_05158_b200.errors import InvalidValue
     with pytest.raises(InvalidValue):
         tg.forward(ix, off, 1, [2048])
+
+
+@pytest.mark.parametrize("optim", ["rowwise_adagrad", "sgd"])
+def test_hybrid_tables_match_full_hbm(mods, optim):
+    """Tables split by rows between HBM and the host tier (HybridTableGroup):
+    pooled outputs are the two part sums (row-wise-shard rounding, f32
+    tolerance), updated weights and optimizer state bitwise equal to the
+    whole tables in HBM; the host part spills when its sets overflow."""
+    tbe, tier = mods
+    rows, dims, hbm_rows, B, steps = [50000, 30000, 7000], [128, 64, 32], [30000, 8000, 6999], 384, 3
+    T = len(rows)
+    rng = np.random.default_rng(29)
+    init = [rng.standard_normal((r, d)).astype(np.float32) for r, d in zip(rows, dims)]
+    full = tbe.TableGroup(rows, dims, dtype=torch.float32, optim=optim)
+    for w, v in zip(full.weights, init):
+        w.copy_(torch.from_numpy(v))
+    hy = tier.HybridTableGroup(rows, dims, hbm_rows, num_sets=256, ways=8, optim=optim)
+    for t in range(T):
+        hy.hbm.weights[t].copy_(torch.from_numpy(init[t][:hbm_rows[t]]))
+        hy.host.host_w[t].copy_(torch.from_numpy(init[t][hbm_rows[t]:]))
+    for s in range(steps):
+        lengths = rng.integers(0, 20, size=(T, B))
+        idx = np.concatenate([rng.integers(0, rows[t], int(lengths[t].sum())) for t in range(T)]).astype(np.int32)
+        off = tbe.lengths_to_offsets(torch.from_numpy(lengths.reshape(-1)).cuda())
+        ix = torch.from_numpy(idx).cuda()
+        up = torch.from_numpy(rng.standard_normal((B, sum(dims))).astype(np.float32)).cuda()
+        a = full.forward(ix, off, B)
+        b = hy.forward(ix, off, B)
+        assert torch.allclose(a, b, rtol=1e-5, atol=1e-5), f"pooled outputs, step {s}"
+        full.backward(ix, off, B, up, mode="update", optim=optim, lr=0.05, eps=1e-8,
+                      table_counts=[int(c) for c in lengths.sum(axis=1)])
+        hy.backward(B, up, lr=0.05, eps=1e-8)
+    hy.flush()
+    assert hy.host.stats["spills"] > 0
+    for t in range(T):
+        h = hbm_rows[t]
+        fw = full.weights[t].cpu()
+        assert torch.equal(fw[:h], hy.hbm.weights[t].cpu()), f"table {t} HBM rows"
+        assert torch.equal(fw[h:], hy.host.host_w[t]), f"table {t} host rows"
+        if full.moments[t] is not None:
+            fm = full.moments[t].cpu()
+            assert torch.equal(fm[:h], hy.hbm.moments[t].cpu()) and torch.equal(fm[h:], hy.host.host_m[t])
