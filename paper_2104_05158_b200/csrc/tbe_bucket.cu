@@ -704,7 +704,8 @@ constexpr int kMaxEnt = 96;             // entries per batch (gather4 groups: <=
 constexpr int kRecMax16 = 1 + kMaxRows / 4 + kMaxRows / 16 + kMaxEnt / 4;  // record size bound (16-byte units)
 
 __host__ __device__ __forceinline__ int rec_units(int m, int nent) {
-  return 1 + (m + 3) / 4 + (m + 15) / 16 + (nent + 3) / 4;
+  const unsigned um = (unsigned)m, un = (unsigned)nent;
+  return (int)(1u + ((um + 3u) >> 2) + ((um + 15u) >> 4) + ((un + 3u) >> 2));
 }
 
 // longest row staged by the row kernel; longer rows are updated by the sort kernel
@@ -1074,22 +1075,16 @@ __global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, Seg
 // batching of 32-row chunks from one prefix scan each, and the records.
 
 struct alignas(16) WSmem {
-  uint32_t in[kWCap];        // the bucket's entries (cp.async-staged, buffer order)
-  uint32_t out[kWCap];       // ... sorted by row
+  uint32_t out[kWCap];       // the bucket's entries sorted by row
   uint32_t hist[kBins];      // digit counts, then cursors; after the placement: the batches
   uint16_t rstart[kBins + 2];
 };
-constexpr int kWW = 8;  // warps per CTA
-
-__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+constexpr int kWW = 8;              // warps per CTA
+constexpr int kWR = kWCap / kWarp;  // entries per lane (held in registers)
+static_assert(kWCap % kWarp == 0, "warp-sort capacity");
 
 template <typename W, typename G, int OPT>
-__global__ void __launch_bounds__(kWW* kWarp) bkt_wsort_kernel(Params q, SegParams p) {
+__global__ void __launch_bounds__(kWW* kWarp, 3) bkt_wsort_kernel(Params q, SegParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
@@ -1112,30 +1107,35 @@ __global__ void __launch_bounds__(kWW* kWarp) bkt_wsort_kernel(Params q, SegPara
     }
     return __shfl_sync(full, j, 0);
   };
-  auto stage = [&](int64_t j) {  // the bucket's entries -> sm.in, asynchronously
-    if (j < 0) return;
-    const int64_t b0 = q.bstart[j];
-    const int n = (int)(q.bstart[j + 1] - b0);
-    for (int i = lane; i < n; i += kWarp) cp_async4(&sm.in[i], q.ent + b0 + i);
-  };
   int64_t j = claim();
-  stage(j);
   while (j >= 0) {
     const int64_t jn = claim();  // the next bucket, claimed early (its metadata loads overlap this one)
     const int t = q.btab[j];
     const int sb = q.sbits[t];
     const int64_t bs = q.bstart[j];
     const int n = (int)(q.bstart[j + 1] - bs);
+    // the bucket's entries in registers (buffer order: entry k*32 + lane),
+    // all loads in flight at once; no shared-memory staging buffer, so three
+    // CTAs (24 warps) fit an SM
+    uint32_t e[kWR];
+#pragma unroll
+    for (int k = 0; k < kWR; ++k) {
+      const int i = k * kWarp + lane;
+      e[k] = i < n ? q.ent[bs + i] : 0u;
+    }
     const int nbins = 1 << sb;
     const uint32_t dm = (uint32_t)nbins - 1;
     const int32_t doff = p.dim_offsets[t];
     const int D = p.dim_offsets[t + 1] - doff;
     const int64_t row0 = (int64_t)(j - q.bbase[t]) << sb;
     for (int d = lane; d < nbins; d += kWarp) sm.hist[d] = 0;
-    cp_async_wait_all();
     __syncwarp();
     // 1. digit histogram (counts only: order does not matter here)
-    for (int i = lane; i < n; i += kWarp) atomicAdd(&sm.hist[(sm.in[i] >> bb) & dm], 1u);
+#pragma unroll
+    for (int k = 0; k < kWR; ++k) {
+      if (k * kWarp >= n) break;
+      if (k * kWarp + lane < n) atomicAdd(&sm.hist[(e[k] >> bb) & dm], 1u);
+    }
     __syncwarp();
     // 2. one scan: cursors (exclusive starts) and the touched rows in order
     const int per = (nbins + kWarp - 1) / kWarp;
@@ -1169,19 +1169,21 @@ __global__ void __launch_bounds__(kWW* kWarp) bkt_wsort_kernel(Params q, SegPara
     }
     if (lane == 0) sm.rstart[nrows] = (uint16_t)n;
     __syncwarp();
-    // 3. stable placement (entries arrive in buffer order)
-    for (int i0 = 0; i0 < n; i0 += kWarp) {
-      const int i = i0 + lane;
-      const bool v = i < n;
-      const uint32_t e = v ? sm.in[i] : 0u;
-      const uint32_t d = v ? (e >> bb) & dm : 0xffffffffu;
+    // 3. stable placement (entries arrive in buffer order); the group leader
+    // reserves the slots with one shared atomic
+#pragma unroll
+    for (int k = 0; k < kWR; ++k) {
+      if (k * kWarp >= n) break;
+      const bool v = k * kWarp + lane < n;
+      const uint32_t d = v ? (e[k] >> bb) & dm : 0xffffffffu;
       const unsigned peers = __match_any_sync(full, d);
-      if (v) sm.out[sm.hist[d] + __popc(peers & lt)] = e;
-      __syncwarp();
-      if (v && (peers >> lane) == 1u) sm.hist[d] += (uint32_t)__popc(peers);
-      __syncwarp();
+      const int leader = __ffs(peers) - 1;
+      uint32_t at = 0;
+      if (v && lane == leader) at = atomicAdd(&sm.hist[d], (uint32_t)__popc(peers));
+      at = __shfl_sync(full, at, leader);
+      if (v) sm.out[at + __popc(peers & lt)] = e[k];
     }
-    stage(jn);  // sm.in is free: the next bucket's entries land during the emission below
+    __syncwarp();
     // 4. batches of 32-row chunks (greedy cuts from one prefix scan per chunk);
     // rows longer than a stage go to the hot-row list
     uint32_t* bat = sm.hist;
@@ -1263,23 +1265,48 @@ __global__ void __launch_bounds__(kWW* kWarp) bkt_wsort_kernel(Params q, SegPara
       if (lane == 0) atomicExch(&q.ctr[4], 1);
       nbat = 0;
     }
+    // headers and each record's first unit, lane-parallel over the batches
+    {
+      uint32_t carry = o16;
+      for (int i0 = 0; i0 < nbat; i0 += kWarp) {
+        const int i = i0 + lane;
+        uint32_t sz = 0, w0 = 0;
+        if (i < nbat) {
+          const uint32_t bw = bat[i];
+          const int r0 = (int)(bw >> 8), m = (int)(bw & 0xff);
+          const uint32_t nent = (uint32_t)(sm.rstart[r0 + m] - sm.rstart[r0]);
+          sz = (uint32_t)rec_units(m, (int)nent);
+          w0 = (uint32_t)m | (nent << 8);
+        }
+        uint32_t incl = sz;
+#pragma unroll
+        for (int o = 1; o < kWarp; o <<= 1) {
+          const uint32_t x = __shfl_up_sync(full, incl, o);
+          if (lane >= o) incl += x;
+        }
+        const uint32_t at = carry + incl - sz;
+        if (i < nbat) {
+          q.hdr[hbase + i] = make_uint2(at, sz);
+          *reinterpret_cast<uint4*>(q.rec + (int64_t)at * 4) = make_uint4(w0, (uint32_t)t, 0u, 0u);
+        }
+        carry += __shfl_sync(full, incl, kWarp - 1);
+      }
+    }
     for (int i = 0; i < nbat; ++i) {
       const uint32_t bw = bat[i];
       const int r0 = (int)(bw >> 8), m = (int)(bw & 0xff);
-      const int e0 = sm.rstart[r0], nent = sm.rstart[r0 + m] - e0;
+      const int rs = lane < m ? sm.rstart[r0 + lane] : 0;
+      const int rs1 = lane < m ? sm.rstart[r0 + lane + 1] : 0;
+      const int e0 = __shfl_sync(full, rs, 0);
+      const int nent = __shfl_sync(full, rs1, m - 1) - e0;
       uint32_t* rec = q.rec + (int64_t)o16 * 4;
-      if (lane == 0) {
-        rec[0] = (uint32_t)m | ((uint32_t)nent << 8);
-        rec[1] = (uint32_t)t;
-        q.hdr[hbase + i] = make_uint2(o16, (uint32_t)rec_units(m, nent));
-      }
-      const int rw = 4 + 4 * ((m + 3) / 4);
+      const unsigned mu = (unsigned)m;
+      const int rw = 4 + 4 * (int)((mu + 3u) >> 2);
       if (lane < m) {
-        const int rs = sm.rstart[r0 + lane];
         rec[4 + lane] = (uint32_t)(row0 + ((sm.out[rs] >> bb) & dm));
-        reinterpret_cast<uint8_t*>(rec + rw)[lane] = (uint8_t)(sm.rstart[r0 + lane + 1] - rs);
+        reinterpret_cast<uint8_t*>(rec + rw)[lane] = (uint8_t)(rs1 - rs);
       }
-      uint32_t* bags = rec + rw + 4 * ((m + 15) / 16);
+      uint32_t* bags = rec + rw + 4 * (int)((mu + 15u) >> 4);
       const int n4 = (nent + 3) & ~3;
       for (int jx = lane; jx < n4; jx += kWarp) bags[jx] = sm.out[e0 + min(jx, nent - 1)] & bmask;
       o16 += (uint32_t)rec_units(m, nent);
@@ -1287,7 +1314,6 @@ __global__ void __launch_bounds__(kWW* kWarp) bkt_wsort_kernel(Params q, SegPara
     __syncwarp();
     j = jn;
   }
-  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------------------
