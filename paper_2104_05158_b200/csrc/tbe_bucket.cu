@@ -1633,6 +1633,11 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p,
   const float lr = (float)p.lr, eps = (float)p.eps;
   int s = 0;
   uint32_t fphase = 0;
+  int t_cur = -1, D = 0, wb = 0, mb = 0, gb = 0, nv = 0, lgS = 0, S = 1, R = kWarp, sub = 0, sl = 0;
+  unsigned submask = full;
+  W* wt = nullptr;
+  float* mom = nullptr;
+  float invD = 1.f;
   for (;;) {
     PROF_T(c_w0);
     mbar_wait(&sm.full[g][s], fphase);
@@ -1642,26 +1647,33 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p,
     const int m = mt.m;
     if (m < 0) break;
     const int t = mt.t;
-    const int D = p.dim_offsets[t + 1] - p.dim_offsets[t];
-    const int wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
-    const int mb = OPT == NEO_OPT_ADAGRAD ? D * 4 : 0;  // element-wise state bytes per row
+    if (t != t_cur) {  // batches arrive table-major: per-table values change rarely
+      t_cur = t;
+      D = p.dim_offsets[t + 1] - p.dim_offsets[t];
+      wb = OPT == NEO_OPT_NONE ? 0 : D * (int)sizeof(W);
+      mb = OPT == NEO_OPT_ADAGRAD ? D * 4 : 0;  // element-wise state bytes per row
+      gb = D * (int)sizeof(G);
+      nv = D / kVW;  // 16-byte W vectors per row
+      // S lanes per row (the smallest power of two with S * kLV >= nv), R rows per warp round
+      const int need = (nv + kLV - 1) / kLV;
+      lgS = need <= 1 ? 0 : 32 - __clz(need - 1);
+      S = 1 << lgS;
+      R = kWarp >> lgS;
+      sub = lane >> lgS;
+      sl = lane & (S - 1);
+      submask = S == kWarp ? full : (((1u << S) - 1u) << (sub * S));
+      wt = reinterpret_cast<W*>(OPT == NEO_OPT_NONE ? p.dense_grads[t] : p.weights[t]);
+      mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD) ? reinterpret_cast<float*>(p.moments[t])
+                                                                       : nullptr;
+      invD = 1.0f / (float)D;
+    }
     const uint32_t mlo = mt.mlo;
     const int mspan = (OPT == NEO_OPT_ROWWISE_ADAGRAD && mlo != ~0u)
                           ? (int)(((mt.row[m - 1] | 3u) + 1u - mlo) * 4)
                           : 0;
-    const int gb = D * (int)sizeof(G);
-    const int nv = D / kVW;  // 16-byte W vectors per row
-    int S = 1;
-    while (S * kLV < nv) S <<= 1;
-    const int R = kWarp / S, sub = lane / S, sl = lane % S;
-    const unsigned submask = S == kWarp ? full : (((1u << S) - 1u) << (sub * S));
     const unsigned char* st = sm.data[g][s];
     const unsigned char* gst = st + ((m * (wb + mb) + mspan + 127) & ~127);
-    W* wt = reinterpret_cast<W*>(OPT == NEO_OPT_NONE ? p.dense_grads[t] : p.weights[t]);
-    float* mom = (OPT == NEO_OPT_ROWWISE_ADAGRAD || OPT == NEO_OPT_ADAGRAD) ? reinterpret_cast<float*>(p.moments[t])
-                                                                           : nullptr;
-    const float invD = 1.0f / (float)D;
-    const int rounds = (m + kRC * R - 1) / (kRC * R);
+    const int rounds = (int)((unsigned)((m + kRC * R - 1) >> (5 - lgS)) / (unsigned)kRC);
     for (int rd = 0; rd < rounds; ++rd) {
       const int rr = (rd * kRC + c) * R + sub;
       const bool valid = rr < m;
@@ -1723,12 +1735,15 @@ __global__ void __launch_bounds__(kRT, 1) bkt_rows_kernel(Params q, SegParams p,
       }
       bool live = valid;
       if (OPT == NEO_OPT_ADAGRAD || OPT == NEO_OPT_ROWWISE_ADAGRAD) {
-        // an identically zero gradient leaves the row untouched (embedding.py:223-228)
-        bool nz = false;
+        // an identically zero gradient leaves the row untouched (embedding.py:223-228);
+        // for row-wise AdaGrad a nonzero sum of squares already decides it
+        bool nz = OPT == NEO_OPT_ROWWISE_ADAGRAD && ss != 0.f;
+        if (!nz) {
 #pragma unroll
-        for (int v = 0; v < kLV; ++v)
+          for (int v = 0; v < kLV; ++v)
 #pragma unroll
-          for (int e = 0; e < kVW; ++e) nz |= acc[v][e] != 0.f;
+            for (int e = 0; e < kVW; ++e) nz |= acc[v][e] != 0.f;
+        }
         const unsigned vote = __ballot_sync(full, nz);
         live = live && (vote & submask) != 0u;
       }
