@@ -75,8 +75,8 @@ def workload_name(a) -> str:
 
 def ncu_traffic(kernel):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/r1_traffic.json), or None."""
-    f = ROOT / "profiles" / "r1_traffic.json"
+    (profiles/r2_traffic.json), or None."""
+    f = ROOT / "profiles" / "r2_traffic.json"
     if kernel is None or not f.exists():
         return None
     try:
@@ -482,8 +482,9 @@ def run_b200(a, rank, world):
     if applies:  # streamed segment-walk + optimizer launches (one per sort group)
         ap_ms = float(np.mean([x.elapsed_time(y) for x, y, _, _ in applies]))
         ap_bytes = float(np.mean([bwd_bytes(U_list[t0:t1], N, D, B) for _, _, t0, t1 in applies]))
-        dominant = ("bkt_update_kernel (per-bucket stable row sort + fused sub-warp-per-row reduce + row-wise "
-                    f"AdaGrad, one launch over {applies[0][3] - applies[0][2]} tables)",
+        dominant = ("bkt_rows_kernel (APPLY of the bucketed backward: warp-specialised TMA producer + sub-warp-per-row "
+                    f"reduce + row-wise AdaGrad, one launch over {applies[0][3] - applies[0][2]} tables; "
+                    "plus the hot-row kernel)",
                     ap_bytes / (ap_ms * 1e-3) / 1e9, ap_bytes, ap_ms)
     else:
         dominant = ("tbe_backward (keys+sort+segments+row-wise AdaGrad)", bwd_gbs, bb, bwd_ms)
@@ -498,8 +499,8 @@ def run_b200(a, rank, world):
                    "l2": "inputs larger than L2 (32.8 GB of tables, 537 MB of ids per step, 2 alternating batches)"},
         "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": dominant[1], "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": dominant[1] / peak,
-                     "traffic": ncu_traffic("bkt_update_kernel" if applies else None),
-                     "traffic_source": "profiles/r1_traffic.json (ncu --set full, one launch)",
+                     "traffic": ncu_traffic("bkt_rows_kernel" if applies else None),
+                     "traffic_source": "profiles/r2_traffic.json (ncu --set full, one launch)",
                      "algorithmic_bytes": dominant[2], "ms": dominant[3]},
         "roofline_fwd": {"kernel": "tbe_forward_kernel", "achieved": fwd_gbs, "frac": fwd_gbs / peak, "ms": fwd_ms,
                          "algorithmic_bytes": fb, "traffic": ncu_traffic("tbe_forward_kernel"),
