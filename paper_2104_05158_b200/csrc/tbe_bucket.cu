@@ -1327,7 +1327,7 @@ __global__ void __launch_bounds__(kWW* kWarp, 3) bkt_wsort_kernel(Params q, SegP
 #define NEO_BKT_RG 4
 #endif
 #ifndef NEO_BKT_RC
-#define NEO_BKT_RC 3
+#define NEO_BKT_RC 4
 #endif
 #ifndef NEO_BKT_RS
 #define NEO_BKT_RS 2
