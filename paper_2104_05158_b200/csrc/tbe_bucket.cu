@@ -54,7 +54,10 @@ namespace bkt {
 
 constexpr int kMaxB = 2048;    // row buckets per table (count / scatter shared-memory histograms)
 constexpr int kSMin = 4;       // smallest bucket: 16 rows
-constexpr int kCHB = 2048;     // bags per count / scatter chunk
+#ifndef NEO_BKT_CHB
+#define NEO_BKT_CHB 1024
+#endif
+constexpr int kCHB = NEO_BKT_CHB;  // bags per count / scatter chunk
 constexpr int kScW = 8;        // warps per count / scatter CTA
 #ifndef NEO_BKT_CAP
 #define NEO_BKT_CAP 2048
