@@ -345,7 +345,10 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
   const int64_t p0 = off[wb0], p1 = off[wb1];
   uint32_t* wh = hist + warp * nb;
   // count pass: the next group's ids are in flight while this group's are counted
-  constexpr int kCU = 8;
+#ifndef NEO_BKT_CU
+#define NEO_BKT_CU 8
+#endif
+  constexpr int kCU = NEO_BKT_CU;
   auto ld_id = [&](int64_t p) -> int64_t { return p < p1 ? (int64_t)indices[p] : -1; };
   {
     int64_t cur[kCU];
@@ -386,7 +389,10 @@ __global__ void __launch_bounds__(kScW* kWarp) bkt_scatter_kernel(Params q, cons
   int64_t onext = win_off(bw + kWarp);
   uint32_t orel = (uint32_t)(o64 - obase);
   int64_t wend = bw + kWarp < wb1 ? __shfl_sync(full, onext, 0) : p1;
-  constexpr int kPU = 4;
+#ifndef NEO_BKT_PU
+#define NEO_BKT_PU 4
+#endif
+  constexpr int kPU = NEO_BKT_PU;
   int64_t cur[kPU];
 #pragma unroll
   for (int u = 0; u < kPU; ++u) cur[u] = ld_id(p0 + u * kWarp + lane);
