@@ -95,10 +95,11 @@ struct Params {
   int32_t* tiles;    // scan tile sums
   int32_t* bstart;   // [nb+1]
   int32_t* btab;     // [nb] table of each bucket
-  uint8_t* bkind;    // [nb] 0 empty, 1 warp-sorted, 2 CTA (shared memory), 3 CTA (global scratch)
+  uint8_t* bkind;    // [nb] 0 empty, 1 / 5 warp-sorted (9- / 10-bit rows), 2 CTA (shared memory), 3 CTA (global)
   int32_t* ctal;     // kind-2 buckets
   int32_t* big;      // queued big buckets
   int32_t* ctr;      // [0] CTA claim counter, [1] big-bucket count, [2] kind-2 count, [3] warp claim
+                     // (9-bit buckets), [8] warp claim (10-bit buckets)
                      // counter, [4] capacity overflow, [5] hot rows,
                      // [6..7] one 64-bit counter: batches (low word), record units (high word)
   uint32_t* ent;     // bucketed entries (row_low << bag_bits | bag)
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(1024) bkt_setup_kernel(Params q) {
   __shared__ int wsum[33];
   __shared__ long long s_carry;
   if (threadIdx.x == 0) s_carry = 0;
-  if (threadIdx.x < 8) q.ctr[threadIdx.x] = 0;
+  if (threadIdx.x < 10) q.ctr[threadIdx.x] = 0;
   __syncthreads();
   for (int t0 = 0; t0 < q.T; t0 += 1024) {
     const int t = t0 + threadIdx.x;
@@ -304,11 +305,17 @@ __global__ void __launch_bounds__(256) bkt_classify_kernel(Params q) {
   q.btab[b] = t;
   if (b + 1 == nbt) q.bstart[nbt] = en;
   const int n = en - st;
-  // 1: one warp sorts it (bkt_wsort_kernel); 2: a CTA, in shared memory; 3: a CTA, through global scratch
-  const uint8_t kind = n == 0 ? 0 : (n <= kWCap && q.sbits[t] <= kDigit) ? 1 : (n <= kCap ? 2 : 3);
+  // 1 / 5: one warp sorts it (bkt_wsort_kernel, 2^9 / 2^10 row bins); 2: a CTA, in shared memory;
+  // 3: a CTA, through global scratch
+  const int sb = q.sbits[t];
+  const uint8_t kind = n == 0                            ? 0
+                       : (n <= kWCap && sb <= kDigit)     ? 1
+                       : (n <= kWCap && sb == kDigit + 1) ? 5
+                       : (n <= kCap ? 2 : 3);
   q.bkind[b] = kind;
   if (kind == 3) q.big[atomicAdd(&q.ctr[1], 1)] = (int32_t)b;
   if (kind == 2) q.ctal[atomicAdd(&q.ctr[2], 1)] = (int32_t)b;
+  if (kind == 5) atomicAdd(&q.ctr[9], 1);  // (the 10-bit warp sort exits at once without them)
 }
 
 // ---------------------------------------------------------------------------
@@ -1083,32 +1090,38 @@ __global__ void __launch_bounds__(kUT, 1024 / kUT) bkt_sort_kernel(Params q, Seg
 // touched rows, a stable match_any placement into shared memory, greedy
 // batching of 32-row chunks from one prefix scan each, and the records.
 
+template <int BINS>
 struct alignas(16) WSmem {
   uint32_t out[kWCap];       // the bucket's entries sorted by row
-  uint32_t hist[kBins];      // digit counts, then cursors; after the placement: the batches
-  uint16_t rstart[kBins + 2];
+  uint32_t hist[BINS];       // digit counts, then cursors; after the placement: the batches
+  uint16_t rstart[BINS + 2];
 };
 constexpr int kWW = 8;              // warps per CTA
 constexpr int kWR = kWCap / kWarp;  // entries per lane (held in registers)
 static_assert(kWCap % kWarp == 0, "warp-sort capacity");
 
-template <typename W, typename G, int OPT>
+// BINS = 512: buckets of <= 2^9 rows (kind 1); 1024: 2^10-row buckets (kind 5)
+template <typename W, typename G, int OPT, int BINS>
 __global__ void __launch_bounds__(kWW* kWarp, 3) bkt_wsort_kernel(Params q, SegParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const unsigned full = 0xffffffffu;
   const int warp = threadIdx.x / kWarp, lane = threadIdx.x % kWarp;
-  WSmem& sm = reinterpret_cast<WSmem*>(smem_raw)[warp];
+  WSmem<BINS>& sm = reinterpret_cast<WSmem<BINS>*>(smem_raw)[warp];
+  constexpr uint8_t kKind = BINS == kBins ? 1 : 5;
+  int32_t* const claim_ctr = q.ctr + (BINS == kBins ? 3 : 8);
   const int64_t nbt = q.bbase[q.T];
   const uint32_t bmask = (uint32_t)((1u << q.bag_bits) - 1u);
   const unsigned lt = lanemask_lt();
   const int bb = q.bag_bits;
   auto claim = [&]() -> int64_t {
     int64_t j = -1;
-    if (lane == 0) {
+    // buckets are claimed in bucket (table-major) order: the row kernel's
+    // batch stream then keeps each table's upstream slice L2-resident
+    if (lane == 0 && (BINS == kBins || q.ctr[9] > 0)) {
       for (;;) {
-        const int64_t jj = atomicAdd(&q.ctr[3], 1);
+        const int64_t jj = atomicAdd(claim_ctr, 1);
         if (jj >= nbt) break;
-        if (q.bkind[jj] == 1) {
+        if (q.bkind[jj] == kKind) {
           j = jj;
           break;
         }
@@ -1857,6 +1870,19 @@ static bool encode_gather_map(const SegParams& p, CUtensorMap* map) {
          CUDA_SUCCESS;
 }
 
+template <typename W, typename G, int OPT, int BINS>
+static int launch_wsort(const Params& q, const SegParams& p, int sms, cudaStream_t s) {
+  auto wkern = bkt_wsort_kernel<W, G, OPT, BINS>;
+  const int wsmem = (int)(sizeof(WSmem<BINS>) * kWW);
+  if (cudaFuncSetAttribute(wkern, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem) != cudaSuccess)
+    return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve warp-sort shared memory");
+  int wper = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, wkern, kWW * kWarp, wsmem);
+  if (wper < 1) wper = 1;
+  wkern<<<(unsigned)(sms * wper), kWW * kWarp, wsmem, s>>>(q, p);
+  return dbg(s, BINS == kBins ? "neo_tbe_backward(bucket warp sort)" : "neo_tbe_backward(bucket warp sort, 10-bit)");
+}
+
 template <typename W, typename G, int OPT>
 static int launch_update(const Params& q, const SegParams& p, int sms, cudaStream_t s, bool prepare, bool apply) {
   if (prepare) {
@@ -1870,15 +1896,9 @@ static int launch_update(const Params& q, const SegParams& p, int sms, cudaStrea
     kern<<<(unsigned)(sms * per_sm), kUT, smem, s>>>(q, p);
     int rc = dbg(s, "neo_tbe_backward(bucket sort)");
     if (rc) return rc;
-    auto wkern = bkt_wsort_kernel<W, G, OPT>;
-    const int wsmem = (int)(sizeof(WSmem) * kWW);
-    if (cudaFuncSetAttribute(wkern, cudaFuncAttributeMaxDynamicSharedMemorySize, wsmem) != cudaSuccess)
-      return fail(NEO_E_CUDA, "neo_tbe_backward: cannot reserve warp-sort shared memory");
-    int wper = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wper, wkern, kWW * kWarp, wsmem);
-    if (wper < 1) wper = 1;
-    wkern<<<(unsigned)(sms * wper), kWW * kWarp, wsmem, s>>>(q, p);
-    rc = dbg(s, "neo_tbe_backward(bucket warp sort)");
+    rc = launch_wsort<W, G, OPT, kBins>(q, p, sms, s);
+    if (rc) return rc;
+    rc = launch_wsort<W, G, OPT, 2 * kBins>(q, p, sms, s);
     if (rc) return rc;
   }
   if (apply) {
@@ -1961,7 +1981,7 @@ size_t bkt_workspace(int32_t T, int64_t B, int64_t N, int64_t total_rows, int32_
   b += align256(sizeof(uint8_t) * (nb + 1));             // bucket kinds
   b += align256(sizeof(int32_t) * (nb + 1));             // kind-2 list
   b += align256(sizeof(int32_t) * (nb + 1));             // big-bucket queue
-  b += align256(sizeof(int32_t) * 8);                    // counters
+  b += align256(sizeof(int32_t) * 16);                   // counters
   b += 2 * align256(sizeof(uint32_t) * n1);              // entries + big-bucket scratch
   b += align256(sizeof(uint2) * hdr_cap);                // batch headers
   b += align256((size_t)16 * rec_cap);                   // batch records
@@ -2027,7 +2047,7 @@ int run_bucket_backward(SegParams p, int32_t weight_dtype, int32_t grad_dtype, c
   q.big = reinterpret_cast<int32_t*>(w);
   w += align256(sizeof(int32_t) * (nb + 1));
   q.ctr = reinterpret_cast<int32_t*>(w);
-  w += align256(sizeof(int32_t) * 8);
+  w += align256(sizeof(int32_t) * 16);
   q.ent = reinterpret_cast<uint32_t*>(w);
   w += align256(sizeof(uint32_t) * n1);
   q.ent2 = reinterpret_cast<uint32_t*>(w);

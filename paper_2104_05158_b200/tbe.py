@@ -300,9 +300,9 @@ class TableGroup:
         f32/f16 tables (f32 for DENSE), SUM, every D a multiple of 8 and
         <= 256, 16-byte aligned rows and gradient.  Also routes to the
         pipelined path groups with a table whose row buckets would span more
-        than 2^9 rows or average more than 1280 ids (bkt_setup_kernel's
+        than 2^10 rows or average more than 1280 ids (bkt_setup_kernel's
         rule, at most 2048 buckets per table): those buckets miss the
-        warp-per-bucket sort and take the CTA sort, which is slower than the
+        warp-per-bucket sorts and take the CTA sort, which is slower than the
         pipelined walk (measured on c3 / c5 at 4 GPUs)."""
         if os.environ.get("NEO_BWD_VARIANT") in ("pipe", "stream"):
             return False
@@ -310,7 +310,7 @@ class TableGroup:
             for h, c in zip(self.rows, table_counts):
                 if h and c:
                     sb = _bucket_bits(h, c)
-                    if sb > 9 or c * (1 << sb) > 1280 * h:  # CTA-sorted buckets (see below)
+                    if sb > 10 or c * (1 << sb) > 1280 * h:  # CTA-sorted buckets (see below)
                         return False
         if pooling != "sum" or mode not in ("update", "dense") or self.max_dim > 256 or self.T == 0:
             return False
