@@ -487,6 +487,8 @@ class ShardedEmbedding:
         ev.start("inputs")
         self._exchange_inputs(batches)
         ev.stop("inputs")
+        for st in S:
+            self._route_backward(st)
         if self.transport == "nvlink":
             p0, dp_handle = self._step_nvlink(S[0], lr, eps, upstream_fn, ev)
             if self.lay.dp_tables:
@@ -807,6 +809,19 @@ class ShardedEmbedding:
         gw = self.gwidth[st.rank][g]
         grp.backward(sc["perm_ids"], sc["perm_off"][k0 * n:], n, sc["recv_grad"][g][:n * gw].view(n, gw),
                      mode="update", optim=self.optim, lr=lr, eps=eps, table_counts=sc["shard_counts"][k0:k1])
+
+    def _route_backward(self, st: RankState) -> None:
+        """One backward path for all of a rank's shard groups (the bucketed
+        sort when every shard qualifies, else the pipelined walk), so the
+        per-group launches (NCCL transport, LocalComm) and the single
+        all-shards launch (NVLink transport) compute the same bits."""
+        shards = self.lay.owned[st.rank]
+        counts = st.sc.get("shard_counts", [])
+        ok = all(tbe.bucket_rule(s.num_rows, int(c)) and s.dim % 8 == 0 and s.dim <= 256
+                 for s, c in zip(shards, counts))
+        for grp in list(st.groups or []) + [st.all_group]:
+            if grp is not None:
+                grp.force_bucketed = ok
 
     def _backward_dp(self, st: RankState) -> None:
         sc = st.sc

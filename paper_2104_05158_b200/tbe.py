@@ -95,6 +95,16 @@ def _u64_ptrs(tensors, device) -> torch.Tensor:
                         device=device)
 
 
+def bucket_rule(h: int, n: int) -> bool:
+    """Does a table of h rows with n ids get warp-sorted buckets (<= 2^10
+    rows, <= 1280 ids on average)?  Else the bucketed path would fall back to
+    its CTA sort, slower than the pipelined walk."""
+    if not h or not n:
+        return True
+    sb = _bucket_bits(h, n)
+    return sb <= 10 and n * (1 << sb) <= 1280 * h
+
+
 def _bucket_bits(h: int, n: int, target: int = 1024) -> int:
     """Row bits per bucket bkt_setup_kernel picks for a table of h rows and n
     ids (tbe_bucket.cu: <= 2048 buckets, about `target` ids per bucket)."""
@@ -306,12 +316,12 @@ class TableGroup:
         pipelined walk (measured on c3 / c5 at 4 GPUs)."""
         if os.environ.get("NEO_BWD_VARIANT") in ("pipe", "stream"):
             return False
-        if table_counts is not None and os.environ.get("NEO_BWD_VARIANT") != "bucket":
-            for h, c in zip(self.rows, table_counts):
-                if h and c:
-                    sb = _bucket_bits(h, c)
-                    if sb > 10 or c * (1 << sb) > 1280 * h:  # CTA-sorted buckets (see below)
-                        return False
+        force = getattr(self, "force_bucketed", None)  # a caller's decision for several groups at once
+        if force is False:
+            return False
+        if table_counts is not None and os.environ.get("NEO_BWD_VARIANT") != "bucket" and force is None:
+            if not all(bucket_rule(h, c) for h, c in zip(self.rows, table_counts)):
+                return False  # CTA-sorted buckets (see below)
         if pooling != "sum" or mode not in ("update", "dense") or self.max_dim > 256 or self.T == 0:
             return False
         if self.dtype not in (torch.float32, torch.float16) or (mode == "dense" and self.dtype != torch.float32):
