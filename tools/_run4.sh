@@ -1,4 +1,5 @@
-timeout 1200 python -m pytest tests/test_gpu_dist.py tests/test_gpu_sharded.py tests/test_gpu_bytes.py tests/test_gpu_configs.py tests/test_gpu_dlrm.py tests/test_gpu_dropin.py -x -q 2>&1 | tail -2
-R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 4"
-$R --workload c3 --steps 10 --warmup 3 > gpurun_out/n4_c3.json 2>gpurun_out/n4_c3.err; python tools/bline.py c3 < gpurun_out/n4_c3.json
-$R --workload c5 --steps 10 --warmup 3 > gpurun_out/n4_c5.json 2>gpurun_out/n4_c5.err; python tools/bline.py c5 < gpurun_out/n4_c5.json
+timeout 2200 python -m pytest tests -m gpu -q 2>&1 | tail -2 > gpurun_out/r2_gpu_tests_final.txt; cat gpurun_out/r2_gpu_tests_final.txt
+for w in 2 4; do
+  timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $w --master-addr 127.0.0.1 --master-port 2963$w tests/dist_parity.py > gpurun_out/r2_dist_parity_w$w.txt 2>&1; echo "w$w rc=$?"; grep dist_parity gpurun_out/r2_dist_parity_w$w.txt
+done
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
