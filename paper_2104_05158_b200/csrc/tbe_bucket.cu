@@ -58,7 +58,10 @@ constexpr int kSMin = 4;       // smallest bucket: 16 rows
 #define NEO_BKT_CHB 1024
 #endif
 constexpr int kCHB = NEO_BKT_CHB;  // bags per count / scatter chunk
-constexpr int kScW = 8;        // warps per count / scatter CTA
+#ifndef NEO_BKT_SCW
+#define NEO_BKT_SCW 8
+#endif
+constexpr int kScW = NEO_BKT_SCW;  // warps per count / scatter CTA
 #ifndef NEO_BKT_CAP
 #define NEO_BKT_CAP 2048
 #endif
